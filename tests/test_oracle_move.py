@@ -1,0 +1,152 @@
+"""Pins of the oracle's column absorption, left move and the rotated R/U/D moves
+(SURVEY 8(c) 'Column absorption and move (a10, a11)').
+
+No truncation (every TS keeps n = rows columns, so every V is square orthogonal and
+P = V V^T = I): the new boundary column, contracted along its internal bonds, must equal
+the old column contracted with the inserted column(s) of the lattice.  The inserted
+columns are written out below directly in picture legs for each of the four directions,
+independently of the oracle's rotate-by-relabelling, so these also pin the rotation."""
+import numpy as np
+import pytest
+
+import ctm_inputs as ci
+from oracle import ctm_oracle as O
+
+E = lambda spec, *ops: np.einsum(spec, *ops, optimize="greedy")
+
+
+# --- boundary columns/rows contracted along their internal bonds (storage orders) ---
+def col_left(C1, Tt, Tb, C4):      # C1(d,r) T1(d,k,b,u) T1(d,k,b,u) C4(r,u) -> (R,k,b,m,n,S)
+    return E("xR,yklx,zmny,Sz->RklmnS", C1, Tt, Tb, C4)
+
+
+def col_right(C2, Tt, Tb, C3):     # C2(l,d) T3(u,k,b,d) T3 C3(u,l) -> (L,k,b,m,n,S)
+    return E("Lx,xkly,ymnz,zS->LklmnS", C2, Tt, Tb, C3)
+
+
+def row_up(C1, Tl, Tr, C2):        # C1(d,r) T2(l,k,b,r) T2 C2(l,d) -> (L,k,b,m,n,R)
+    return E("Lx,xkly,ymnz,zR->LklmnR", C1, Tl, Tr, C2)
+
+
+def row_down(C4, Tl, Tr, C3):      # C4(r,u) T4(r,k,b,l) T4 C3(u,l) -> (L,k,b,m,n,R)
+    return E("xL,yklx,zmny,Rz->LklmnR", C4, Tl, Tr, C3)
+
+
+# --- inserting one column/row of the lattice (site legs (s,u,l,d,r)) -------------------
+def ins_left(col, T2, X, Y, T4):   # col (R,k,b,m,n,S); T2(l=R,..,r=R2); T4(r=S2,..,l=S)
+    return E("RkbmnS,RuvQ,sukdK,svbeL,tdmgM,teniN,WgiS->QKLMNW",
+             col, T2, X, X, Y, Y, T4)
+
+
+def ins_right(col, T2, X, Y, T4):  # col (L,k,b,m,n,S); T2(l=Q, r=L); T4(r=S, l=W)
+    return E("LkbmnS,QuvL,suKdk,svPeb,tdMgm,teNin,SgiW->QKPMNW",
+             col, T2, X, X, Y, Y, T4)
+
+
+def ins_up(row, T1, X, Y, T3):     # row (L,k,b,m,n,R); T1(d=Q, u=L); T3(u=R, d=W)
+    return E("LkbmnR,QpqL,skpKr,sbqPv,tmrMw,tnvNx,RwxW->QKPMNW",
+             row, T1, X, X, Y, Y, T3)
+
+
+def ins_down(row, T1, X, Y, T3):   # row (L,k,b,m,n,R); T1(d=L, u=Q); T3(u=W, d=R)
+    return E("LkbmnR,LpqQ,sKpkr,sPqbv,tMrmw,tNvnx,WwxR->QKPMNW",
+             row, T1, X, X, Y, Y, T3)
+
+
+def _nrm(x):
+    return x / np.linalg.norm(x)
+
+
+def _env(cfg):
+    g = ci.generate(cfg)
+    return {"C": g["C"], "T": g["T"]}, g["A"], g["B"]
+
+
+def _expected_and_got(env, new, A, B, direction, x):
+    y = O.OTHER[x]
+    S = {"a": A, "b": B}
+    C, T = env["C"], env["T"]
+    nC, nT = new["C"], new["T"]
+    if direction == "left":
+        old = col_left(C[(x, 1)], T[(x, 1)], T[(y, 1)], C[(y, 4)])
+        exp = ins_left(ins_left(old, T[(x, 2)], S[x], S[y], T[(y, 4)]), T[(y, 2)], S[y], S[x], T[(x, 4)])
+        got = col_left(nC[(x, 1)], nT[(x, 1)], nT[(y, 1)], nC[(y, 4)])
+    elif direction == "right":
+        old = col_right(C[(x, 2)], T[(x, 3)], T[(y, 3)], C[(y, 3)])
+        exp = ins_right(ins_right(old, T[(x, 2)], S[x], S[y], T[(y, 4)]), T[(y, 2)], S[y], S[x], T[(x, 4)])
+        got = col_right(nC[(x, 2)], nT[(x, 3)], nT[(y, 3)], nC[(y, 3)])
+    elif direction == "up":
+        old = row_up(C[(x, 1)], T[(x, 2)], T[(y, 2)], C[(y, 2)])
+        exp = ins_up(ins_up(old, T[(x, 1)], S[x], S[y], T[(y, 3)]), T[(y, 1)], S[y], S[x], T[(x, 3)])
+        got = row_up(nC[(x, 1)], nT[(x, 2)], nT[(y, 2)], nC[(y, 2)])
+    else:
+        old = row_down(C[(x, 4)], T[(x, 4)], T[(y, 4)], C[(y, 3)])
+        exp = ins_down(ins_down(old, T[(x, 1)], S[x], S[y], T[(y, 3)]), T[(y, 1)], S[y], S[x], T[(x, 3)])
+        got = row_down(nC[(x, 4)], nT[(x, 4)], nT[(y, 4)], nC[(y, 3)])
+    return _nrm(exp), _nrm(got)
+
+
+@pytest.mark.parametrize("direction", ["left", "right", "up", "down"])
+def test_full_move_without_truncation_is_exact(direction):
+    """chi0 = 1 -> 4 -> 16 over a full move (both absorptions keep n = rows)."""
+    cfg = ci.custom(2, 2, 16, chi0=1, seed_index=21)
+    env, A, B = _env(cfg)
+    new = O.move(env, A, B, direction, 16)
+    for x in ("a", "b"):
+        exp, got = _expected_and_got(env, new, A, B, direction, x)
+        assert exp.shape == got.shape
+        assert np.allclose(got, exp, atol=1e-12), np.abs(got - exp).max()
+
+
+@pytest.mark.parametrize("direction", ["left", "right", "up", "down"])
+def test_D1_move_is_exact(direction):
+    cfg = ci.custom(2, 1, 3, seed_index=22)
+    env, A, B = _env(cfg)
+    new = O.move(env, A, B, direction, 3)
+    for x in ("a", "b"):
+        exp, got = _expected_and_got(env, new, A, B, direction, x)
+        assert np.allclose(got, exp, atol=1e-12)
+
+
+def test_single_absorption_chi0_4_to_16_is_exact():
+    cfg = ci.custom(2, 2, 16, chi0=4, seed_index=23)
+    env, A, B = _env(cfg)
+    new, proj = O.column_absorption(env, A, B, 16)
+    S = {"a": A, "b": B}
+    C, T, nC, nT = env["C"], env["T"], new["C"], new["T"]
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        v = proj[x + y]["v2"]
+        assert v.shape[-1] == 16 and v.shape[0] * v.shape[1] == 16      # square: P = I
+        old = col_left(C[(x, 1)], T[(x, 1)], T[(y, 1)], C[(y, 4)])
+        exp = ins_left(old, T[(x, 2)], S[x], S[y], T[(y, 4)])
+        got = col_left(nC[(y, 1)], nT[(y, 1)], nT[(x, 1)], nC[(x, 4)])
+        assert np.allclose(_nrm(got), _nrm(exp), atol=1e-12)
+
+
+def test_sequential_full_chi_prime_absorption_equals_reduced():
+    """With chi' = chi0 D (v1 square) and chi'' = chi0 D^2 (exact reduced env), the
+    sequential projectors equal the REDUCED ones, so the gauge-invariant
+    contracted columns of one truncating absorption agree."""
+    cfg = ci.custom(2, 2, 3, chi0=4, seed_index=24)
+    env, A, B = _env(cfg)
+    seq, _ = O.column_absorption(env, A, B, 3, chi_p=8, chi_pp=16, strategy="sequential")
+    red, _ = O.column_absorption(env, A, B, 3, strategy="reduced")
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        cs = col_left(seq["C"][(y, 1)], seq["T"][(y, 1)], seq["T"][(x, 1)], seq["C"][(x, 4)])
+        cr = col_left(red["C"][(y, 1)], red["T"][(y, 1)], red["T"][(x, 1)], red["C"][(x, 4)])
+        assert np.allclose(_nrm(cs), _nrm(cr), atol=1e-10)
+
+
+def test_truncating_move_shapes_and_isometries():
+    cfg = ci.CONFIGS["tiny"]
+    env, A, B = _env(cfg)
+    stats = []
+    new = O.left_move(env, A, B, cfg.chi, stats=stats)
+    for k, v in new["C"].items():
+        assert v.shape == (8, 8)
+        assert np.isclose(np.linalg.norm(v), 1.0) or k[1] in (2, 3)
+    for k, v in new["T"].items():
+        assert v.shape == (8, 2, 2, 8)
+    assert all(np.isfinite(s["gap"]) or s["gap"] == np.inf for s in stats)
