@@ -1,0 +1,210 @@
+/*
+ * ctm.h -- C ABI of libctm: the CTMRG move of arXiv 2306.08212 (Lan & Evenbly,
+ * "Reduced Contraction Costs of Corner-Transfer Methods for PEPS") on one B200, FP64.
+ *
+ * Citations: "P:Lnn" = PAPER.md line nn.  SURVEY.md sections 0 and 8 fix the readings
+ * (listed in DESIGN.md "Readings").
+ *
+ * ---------------------------------------------------------------------------------
+ * Conventions common to every call
+ * ---------------------------------------------------------------------------------
+ *  Tensors.  Every tensor argument is a DEVICE pointer to contiguous row-major float64
+ *    memory, owned by the caller.  The library never frees or retains caller memory
+ *    past the call.  Shapes follow the paper's definitions:
+ *      site A, B           (d, D, D, D, D)  legs (s, u, l, d, r)            [P:L39]
+ *      corner C_x^k        (chi, chi)                                      [P:L41]
+ *      edge   T_x^k        (chi, D, D, chi)  (boundary, ket, bra, boundary) [P:L41]
+ *    Environment tensors are stored walking the boundary clockwise:
+ *      T^1 (d,k,b,u)  T^2 (l,k,b,r)  T^3 (u,k,b,d)  T^4 (r,k,b,l)
+ *      C^1 (d,r)      C^2 (l,d)      C^3 (u,l)      C^4 (r,u)
+ *    where k/b are the ket/bra legs facing the bulk (kept split).
+ *    The bra layer is passed separately (Xbra) but all shipped configs are real.
+ *  Isometries (Fig 4): v1 (chi_in, D, chi') and v2 (chi', D, chi_out),
+ *    row-major, i.e. the first chi' (resp. chi_out) left singular vectors of the
+ *    (chi D) x (D chi) and (chi' D) x chi matrices, columns sign-fixed so that the
+ *    largest-|.| entry of each column is positive (ties: lowest row index).
+ *  Stream.  All work is enqueued on the stream given to ctm_init (a cudaStream_t
+ *    passed as uintptr_t; 0 = legacy default stream; ctm_set_stream changes it).
+ *    Calls that run SVDs synchronise that stream (cuSOLVER status and host-side
+ *    error checks); pure-contraction calls are asynchronous.
+ *  Workspace.  ctm_init reports the bytes needed; the caller allocates device memory
+ *    (e.g. a torch tensor) and hands it over with ctm_set_workspace before any compute
+ *    call.  The handle owns only cuSOLVER/cuBLAS-free state (solver handle, events).
+ *  Errors.  Every call returns an int status (below).  No C++ exception crosses the
+ *    ABI.  ctm_last_error(h) returns a NUL-terminated message for the last failure of
+ *    that handle (valid until the next call on it).  A failed call leaves output
+ *    buffers unspecified; ctm_left_move commits the environment only after every
+ *    check of the move passed (snapshot semantics).
+ */
+#ifndef CTM_H_
+#define CTM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CTM_ABI_VERSION 1
+
+/* status codes */
+#define CTM_OK 0
+#define CTM_E_ARG 1          /* null pointer, bad extent, missing workspace          */
+#define CTM_E_CUDA 2         /* CUDA runtime / launch failure                         */
+#define CTM_E_SOLVER 3       /* SVD failed to converge (message carries m x n) */
+#define CTM_E_NONFINITE 4    /* NaN/Inf produced (message names absorption, tensor)  */
+#define CTM_E_NOMEM 5        /* workspace too small                                   */
+#define CTM_E_UNSUPPORTED 6  /* strategy / mode not built in this library             */
+#define CTM_W_CLAMPED 100    /* warning bit: chi' > chi D was clamped        */
+
+/* strategies (ctm_params.strategy) */
+#define CTM_SEQUENTIAL 0     /* reduced env + sequential ket/bra order: the hot path  */
+#define CTM_REDUCED_EXACT 1  /* NEXT on the GPU (oracle only in round 1)               */
+
+/* SVD back-ends (ctm_params.svd_algo); all on the device, no CPU fallback */
+#define CTM_SVD_GESVDP 0     /* cuSOLVER Xgesvdp (polar decomposition), default       */
+#define CTM_SVD_GESVDJ 1     /* cuSOLVER gesvdj (Jacobi), tolerance svd_tol            */
+#define CTM_SVD_GESVD 2      /* cuSOLVER Xgesvd (QR iteration)                         */
+
+/* flags (ctm_params.flags) */
+#define CTM_FLAG_CHECK_FINITE 1   /* scan every committed tensor for NaN/Inf         */
+
+/* reduced-env modes (ctm_reduced_env) */
+#define CTM_RENV_APPROX 0    /* {C'^1, T'^2, C'^2} with side isometries */
+#define CTM_RENV_EXACT 1     /* exact Fig 3(b) network, P:L53 (NEXT on GPU)            */
+
+/* bonds (ctm_bond_energy) */
+#define CTM_BOND_H 0         /* A left of B: 2x1 window                               */
+#define CTM_BOND_V 1         /* A above B: 1x2 window                                 */
+
+/* directions (ctm_move) */
+#define CTM_LEFT 0
+#define CTM_RIGHT 1
+#define CTM_UP 2
+#define CTM_DOWN 3
+
+typedef struct ctm_handle_s* ctm_handle;
+
+typedef struct {
+  int d;           /* physical dimension                                       */
+  int D;           /* virtual bond dimension                                   */
+  int chi;         /* boundary dimension chi                                   */
+  int chi_p;       /* chi'  : first sequential isometry                        */
+  int chi_pp;      /* chi'' : appendix side isometries v_l, v_r               */
+  int strategy;    /* CTM_SEQUENTIAL                                                   */
+  int svd_algo;    /* CTM_SVD_*                                                        */
+  double svd_tol;  /* gesvdj tolerance (<= 0: machine epsilon)                         */
+  int flags;       /* CTM_FLAG_*                                                       */
+} ctm_params;
+
+/* The 16 environment tensors (C_x^k, T_x^k, x in {a,b}, k = 1..4) and their
+ * boundary extents.  C[x][k-1], T[x][k-1] with x = 0 for 'a', 1 for 'b'.
+ * ext[x][j][0..1] = (first, last) boundary extent in STORAGE order, j = 0..3 for
+ * C^1..C^4 and j = 4..7 for T^1..T^4.  Buffers must be allocated with capacity for the
+ * target extents (chi x chi, chi x D x D x chi); moves update ext in place. */
+typedef struct {
+  double* C[2][4];
+  double* T[2][4];
+  int ext[2][8][2];
+} ctm_env;
+
+/* Per-call statistics (host struct, filled by ctm_left_move / ctm_move). */
+typedef struct {
+  double ms_total;      /* device time of the call (CUDA events)                       */
+  double ms_svd;        /* device time inside the SVD stages (cuSOLVER + sign fix)      */
+  double ms_contract;   /* ms_total - ms_svd                                           */
+  double flops;         /* algorithmic contraction flops (SURVEY 8(a) closed form)      */
+  double min_gap;       /* min sigma_n / sigma_{n+1} over every truncation of the call  */
+  int n_svd;            /* SVDs run                                                    */
+  int n_kernels;        /* libctm kernels launched (excluding cuSOLVER internals)       */
+} ctm_move_stats;
+
+/* ctm_init: validate sizes, create the handle, report the workspace bytes needed by
+ * every call for these params (the peak of SURVEY 8(a): intermediates of two
+ * concurrent absorb chains + SVD buffers).  Env initialisation is NOT done here: the
+ * seeded generator lives in the harness (ctm_inputs.py) so the oracle and the GPU see
+ * bit-identical inputs.  Returns CTM_E_ARG for d, D, chi < 1. */
+int ctm_init(ctm_handle* h, const ctm_params* p, uintptr_t stream, size_t* ws_bytes);
+int ctm_set_workspace(ctm_handle h, void* dev, size_t bytes);
+int ctm_set_stream(ctm_handle h, uintptr_t stream);
+int ctm_destroy(ctm_handle h);
+const char* ctm_last_error(ctm_handle h);
+int ctm_abi_version(void);
+
+/* ctm_reduced_env: SURVEY rows a1-a4 (Fig 3(c), appendix).
+ * Inputs (all chi = params.chi):  C1 = C_x^1 (d,r); T2 = T_x^2 (l,k,b,r);
+ * C2 = C_x^2 (l,d); T1 = T_x^1 (d,k,b,u); X, Xbra = site x (s,u,l,d,r);
+ * T3 = T_x^3 (u,k,b,d).
+ * Output M_out (chi, D, D, chi) = M(q, k_d, b_d, q') with q = T^1's d leg,
+ * (k_d, b_d) = X's down legs, q' = T^3's d leg.  M is gauge-free (its legs are
+ * existing bonds).  mode CTM_RENV_APPROX: M = C'^1 T'^2 C'^2 with side isometries
+ * (v_l1, v_l2) = TS(C^1 T^1; chi'', chi''), (v_r1, v_r2) = TS(C^2 T^3; chi'', chi'').
+ * iso_out (nullable) receives vl1, vl2, vr1, vr2 back to back (shapes
+ * (chi,D,n1), (n1,D,n2) twice, n1 = min(chi'', chi D), n2 = min(chi'', n1 D)).
+ * Synchronises the stream (SVDs). */
+int ctm_reduced_env(ctm_handle h, const double* C1, const double* T2, const double* C2,
+                    const double* T1, const double* X, const double* Xbra, const double* T3,
+                    int mode, double* M_out, double* iso_out);
+
+/* ctm_absorb_truncate: SURVEY rows a6-a8 (Fig 4(b)): ket absorption,
+ * v1 truncation, bra absorption, v2 truncation, in six contractions S1..S6.
+ *   T      (chi, D, D, chi)      as (in, k_face, b_face, out)
+ *   X, Xbra(d, D, D, D, D)       as (s, in, face, out, far)   (chain orientation)
+ *   v1_in  (chi, D, chi'), v2_in (chi', D, chi)   isometry of the cut on the in side
+ *   v1_out (chi, D, chi'), v2_out(chi', D, chi)   isometry of the cut on the out side
+ *   T_out  (chi, D, D, chi)      as (o1, k_far, b_far, o2), NOT normalised.
+ * Asynchronous. */
+int ctm_absorb_truncate(ctm_handle h, const double* T, const double* X, const double* Xbra,
+                        const double* v1_in, const double* v2_in, const double* v1_out,
+                        const double* v2_out, double* T_out);
+
+/* ctm_left_move: SURVEY rows a1-a11: two column absorptions, projectors
+ * recomputed for each (reading R4); each absorption updates C_a^1, C_b^1, T_a^1,
+ * T_b^1, C_a^4, C_b^4 from one snapshot (reading R3) and Frobenius-normalises them
+ * (reading R13).  A, B (d,D,D,D,D) as (s,u,l,d,r).
+ * iso_in (nullable): inject the main isometries instead of computing them (no reduced
+ *   env, no SVD: the contraction-only path).  Layout: for absorption a = 0,1 and cut
+ *   c = ab, ba: v1 (chi, D, chi') then v2 (chi', D, chi), back to back.
+ * iso_out (nullable): receives the isometries used, same layout.
+ * iso_in / iso_out require all env extents == chi.
+ * st (nullable, host): timing and statistics. */
+int ctm_left_move(ctm_handle h, const double* A, const double* B, ctm_env* env,
+                  const double* iso_in, double* iso_out, ctm_move_stats* st);
+
+/* ctm_move: the move in direction dir (CTM_LEFT/RIGHT/UP/DOWN) = relabel the
+ * environment by quarter turns (clockwise storage: no data movement), permute the
+ * site legs on the device, left move, turn back ("moves in other directions
+ * can be adjusted accordingly").  ctm_iterate runs n_iter x (left, right, up, down). */
+int ctm_move(ctm_handle h, int dir, const double* A, const double* B, ctm_env* env,
+             ctm_move_stats* st);
+int ctm_iterate(ctm_handle h, const double* A, const double* B, ctm_env* env, int n_iter,
+                ctm_move_stats* st);
+
+/* ctm_norm_2x2: <psi|psi> closed on the 2x2 patch of Fig 1(d):
+ *     C_a^1 T_a^2 T_b^2 C_b^2 / T_a^1 A B T_b^3 / T_b^1 B A T_a^3 / C_b^4 T_b^4 T_a^4 C_a^3
+ * = Tr(E_ul E_ur E_lr E_ll).  out_host: the value.  cancel_ratio_host (nullable): the
+ * value divided by the same closure over entrywise |.| (conditioning report).
+ * Synchronises the stream. */
+int ctm_norm_2x2(ctm_handle h, const double* A, const double* B, const ctm_env* env,
+                 double* out_host, double* cancel_ratio_host);
+
+/* ctm_bond_energy: two-site reduced density matrix on the 2x1 (CTM_BOND_H) or 1x2
+ * (CTM_BOND_V) window, symmetrised (rho + rho^T)/2 and trace-normalised;
+ * e = Tr(rho h) with h (d,d,d,d) = <s_i s_j| h |s_i' s_j'> on the device.
+ * rho_out (nullable, device): (d,d,d,d) as (s_A, s_B, t_A, t_B).
+ * e_out_host: the energy.  Synchronises the stream. */
+int ctm_bond_energy(ctm_handle h, const double* A, const double* B, const ctm_env* env,
+                    const double* hop, int bond, double* rho_out, double* e_out_host);
+
+/* Algorithmic FP64 flops of one left move for square extents (SURVEY 8(a) closed form):
+ * F_move = 2 (2 F_renv + 2 F_chain + 4 F_corner). */
+double ctm_move_flops(int d, int D, int chi, int chi_p, int chi_pp);
+
+/* Number of libctm kernels launched since the handle was created (evidence counter). */
+int64_t ctm_kernel_count(ctm_handle h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CTM_H_ */

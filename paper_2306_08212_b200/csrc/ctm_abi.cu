@@ -1,0 +1,839 @@
+// ctm_abi.cu -- libctm: the C ABI of include/ctm.h and the CTMRG move driver.
+//
+// Every contraction of the move runs in tc_gemm (FP64 DMMA, permutations fused into the
+// loads), every SVD on the device (svd.cu), every elementwise step in kernels.cu.  The
+// host code here only plans shapes, walks the paper's steps and checks statuses.
+//
+// Citations: P:Lnn = PAPER.md line; rows a1..a11 and S1..S6 = SURVEY.md 8(a).
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <memory>
+
+#include "ctm_internal.h"
+
+namespace ctm {
+namespace {
+
+// ---------------------------------------------------------------------------------------
+// small tensor views
+// ---------------------------------------------------------------------------------------
+struct Ten {
+  double* p = nullptr;
+  std::vector<int> ext;
+  size_t size() const {
+    size_t n = 1;
+    for (int e : ext) n *= (size_t)e;
+    return n;
+  }
+};
+
+Operand op(const std::vector<const Ten*>& ts, const char* lab) {
+  Operand o;
+  o.lab = lab;
+  o.ext = ts[0]->ext;
+  for (auto* t : ts) o.p.push_back(t->p);
+  return o;
+}
+OutOperand out(const std::vector<Ten*>& ts, const char* lab, const std::vector<double*>& ss = {}) {
+  OutOperand o;
+  o.lab = lab;
+  o.ext = ts[0]->ext;
+  for (auto* t : ts) o.p.push_back(t->p);
+  o.sumsq = ss;
+  return o;
+}
+Ten alloc(Handle& h, std::vector<int> ext) {
+  Ten t;
+  t.ext = std::move(ext);
+  t.p = h.ws.take(t.size());
+  return t;
+}
+
+// Site tensor in the two orientations the chain needs (S2 / S5 operands).
+struct Site {
+  Ten ket;   // (in, face, s, out, far)            "ifsoz"
+  Ten bra;   // (s, face, in, out, far)            "sgjyw"
+};
+
+// X (s,u,l,d,r) -> chain orientation given by the source axes of (in, face, out, far).
+Site make_site(Handle& h, const double* X, const double* Xb, int d, int D, int in, int face, int outl, int far) {
+  Site s;
+  s.ket = alloc(h, {D, D, d, D, D});
+  s.bra = alloc(h, {d, D, D, D, D});
+  if (!h.dry) {
+    permute(h, X, {d, D, D, D, D}, {in, face, 0, outl, far}, s.ket.p);
+    permute(h, Xb, {d, D, D, D, D}, {0, face, in, outl, far}, s.bra.p);
+  }
+  return s;
+}
+// (s,u,l,d,r) axes: s=0 u=1 l=2 d=3 r=4
+Site site_left(Handle& h, const double* X, int d, int D) { return make_site(h, X, X, d, D, 3, 2, 1, 4); }
+Site site_top(Handle& h, const double* X, int d, int D) { return make_site(h, X, X, d, D, 2, 1, 4, 3); }
+
+struct Iso {
+  Ten v1, v2;   // v1 (P, D, n1), v2 (n1, D, n2)
+};
+
+// ---------------------------------------------------------------------------------------
+// Rows a6-a8: sequential absorb/truncate chain S1..S6 (Fig 4(b)).
+// Batched over jobs with identical shapes.
+// ---------------------------------------------------------------------------------------
+struct ChainJob {
+  const Ten* T;          // (cin, D, D, cout) as (in, face_k, face_b, out)
+  const Site* X;
+  const Iso* in;         // v1 (cin, D, n1), v2 (n1, D, o1)
+  const Iso* outv;       // v1 (cout, D, m1), v2 (m1, D, o2)
+  Ten* res;              // (o1, D, D, o2), allocated by the caller
+  double* ss;            // nullable: fused sum of squares of res
+};
+
+void chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
+  const int B = (int)jobs.size();
+  const ChainJob& j0 = jobs[0];
+  const int D = j0.T->ext[1];
+  const int d = j0.X->bra.ext[0];
+  const int cout = j0.T->ext[3];
+  const int n1 = j0.in->v1.ext[2], o1 = j0.in->v2.ext[2];
+  const int m1 = j0.outv->v1.ext[2], o2 = j0.outv->v2.ext[2];
+  const size_t mark = h.ws.top;
+  std::vector<Ten> X1(B), X2(B), X3(B), X4(B), X5(B);
+  for (int b = 0; b < B; ++b) {
+    // buf1 holds X1 / X3 / X5, buf2 holds X2 / X4 (lifetimes do not overlap)
+    size_t s1 = std::max({(size_t)D * n1 * D * D * cout, (size_t)n1 * D * d * D * m1, (size_t)m1 * D * D * D * o1});
+    size_t s2 = std::max((size_t)n1 * D * d * D * D * cout, (size_t)d * D * D * D * m1 * o1);
+    double* b1 = h.ws.take(s1);
+    double* b2 = h.ws.take(s2);
+    X1[b] = {b1, {D, n1, D, D, cout}};
+    X2[b] = {b2, {n1, D, d, D, D, cout}};
+    X3[b] = {b1, {n1, D, d, D, m1}};
+    X4[b] = {b2, {d, D, D, D, m1, o1}};
+    X5[b] = {b1, {m1, D, D, D, o1}};
+  }
+  auto P = [&](auto f) {
+    std::vector<const Ten*> v;
+    for (int b = 0; b < B; ++b) v.push_back(f(b));
+    return v;
+  };
+  auto Q = [&](std::vector<Ten>& t) {
+    std::vector<Ten*> v;
+    for (int b = 0; b < B; ++b) v.push_back(&t[b]);
+    return v;
+  };
+  std::vector<Ten*> res;
+  std::vector<double*> ss;
+  for (auto& j : jobs) {
+    res.push_back(j.res);
+    if (j.ss) ss.push_back(j.ss);
+  }
+  if (!ss.empty() && (int)ss.size() != B) throw Error(CTM_E_ARG, "chain: partial sumsq");
+  // S1: X1(i,a,f,g,q) = sum_p v1_in(p,i,a) T(p,f,g,q)                     K = chi
+  contract(h, op(P([&](int b) { return &jobs[b].in->v1; }), "pia"), op(P([&](int b) { return jobs[b].T; }), "pfgq"),
+           out(Q(X1), "iafgq"));
+  // S2: X2(a,g,s,z,o,q) = sum_{i,f} X1(i,a,f,g,q) X(i,f,s,o,z)               K = D^2
+  contract(h, op(P([&](int b) { return (const Ten*)&X1[b]; }), "iafgq"),
+           op(P([&](int b) { return &jobs[b].X->ket; }), "ifsoz"), out(Q(X2), "agszoq"));
+  // S3: X3(a,g,s,z,b) = sum_{q,o} X2(a,g,s,z,o,q) v1_out(q,o,b)               K = chi D
+  contract(h, op(P([&](int b) { return (const Ten*)&X2[b]; }), "agszoq"),
+           op(P([&](int b) { return &jobs[b].outv->v1; }), "qob"), out(Q(X3), "agszb"));
+  // S4: X4(s,g,j,z,b,c) = sum_a X3(a,g,s,z,b) v2_in(a,j,c)                   K = chi'
+  contract(h, op(P([&](int b) { return (const Ten*)&X3[b]; }), "agszb"),
+           op(P([&](int b) { return &jobs[b].in->v2; }), "ajc"), out(Q(X4), "sgjzbc"));
+  // S5: X5(b,y,z,w,c) = sum_{s,g,j} X4(s,g,j,z,b,c) X*(s,g,j,y,w)            K = d D^2
+  contract(h, op(P([&](int b) { return (const Ten*)&X4[b]; }), "sgjzbc"),
+           op(P([&](int b) { return &jobs[b].X->bra; }), "sgjyw"), out(Q(X5), "byzwc"));
+  // S6: T'(c,z,w,d) = sum_{b,y} X5(b,y,z,w,c) v2_out(b,y,d)                  K = chi' D
+  contract(h, op(P([&](int b) { return (const Ten*)&X5[b]; }), "byzwc"),
+           op(P([&](int b) { return &jobs[b].outv->v2; }), "byd"), out(res, "czwd", ss));
+  h.ws.reset(mark);
+}
+
+bool same_shapes(const ChainJob& a, const ChainJob& b) {
+  return a.T->ext == b.T->ext && a.in->v1.ext == b.in->v1.ext && a.in->v2.ext == b.in->v2.ext &&
+         a.outv->v1.ext == b.outv->v1.ext && a.outv->v2.ext == b.outv->v2.ext;
+}
+
+void chains(Handle& h, const std::vector<ChainJob>& jobs) {
+  if (jobs.size() == 2 && same_shapes(jobs[0], jobs[1])) {
+    chain_batch(h, jobs);
+  } else {
+    for (auto& j : jobs) chain_batch(h, {j});
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Row a2 / a5: two-stage isometry TS(Q; c1, c2).
+//   Q (P, D, D, F) as (boundary, ket, bra, far); returns v1 (P, D, n1), v2 (n1, D, n2) and
+//   optionally Q2 = v1^T Q (n1, D, F), which the reduced env reuses for C' (row a4).
+// ---------------------------------------------------------------------------------------
+Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep) {
+  const int P = Qt.ext[0], K = Qt.ext[1], Bd = Qt.ext[2], F = Qt.ext[3];
+  const int n1 = std::min(c1, P * K);
+  Iso r;
+  r.v1 = alloc(h, {P, K, n1});
+  svd_left(h, Qt.p, P * K, Bd * F, n1, r.v1.p);
+  Ten Q2 = alloc(h, {n1, Bd, F});
+  contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
+  const int n2 = std::min(c2, n1 * Bd);
+  r.v2 = alloc(h, {n1, Bd, n2});
+  svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p);
+  if (Q2_keep) *Q2_keep = Q2;
+  return r;
+}
+
+// ---------------------------------------------------------------------------------------
+// Rows a1-a4: approximated reduced environment M = C'^1 T'^2 C'^2 (Fig 3(c),
+// appendix).  Batched over the two cut types when shapes agree.
+// ---------------------------------------------------------------------------------------
+struct RenvIn {
+  Ten C1, T2, C2, T1, T3;   // storage orders C1 (d,r), T2 (l,k,b,r), C2 (l,d), T1 (d,k,b,u), T3 (u,k,b,d)
+  const Site* X;            // top orientation
+};
+struct RenvOut {
+  Ten M;                    // (q, k, b, q')
+  Iso vl, vr;
+};
+
+RenvOut reduced_env(Handle& h, const RenvIn& in, int chi_pp) {
+  RenvOut o;
+  const int D = in.T1.ext[1];
+  // a1: Q_l(p,k,b,q) = sum_x C1(x,p) T1(q,k,b,x);  Q_r(p,k,b,q) = sum_x C2(p,x) T3(x,k,b,q)
+  Ten Ql = alloc(h, {in.C1.ext[1], D, D, in.T1.ext[0]});
+  Ten Qr = alloc(h, {in.C2.ext[0], D, D, in.T3.ext[3]});
+  contract(h, op({&in.C1}, "xp"), op({&in.T1}, "qkbx"), out({&Ql}, "pkbq"));
+  contract(h, op({&in.C2}, "px"), op({&in.T3}, "xkbq"), out({&Qr}, "pkbq"));
+  // a2: side isometries (v_l^1, v_l^2), (v_r^1, v_r^2) = TS(Q; chi'', chi'')
+  Ten Q2l, Q2r;
+  o.vl = ts_isometry(h, Ql, chi_pp, chi_pp, &Q2l);
+  o.vr = ts_isometry(h, Qr, chi_pp, chi_pp, &Q2r);
+  // a3: T'^2 = chain(T^2, X top orientation, in = v_l, out = v_r)
+  Ten Tp = alloc(h, {o.vl.v2.ext[2], D, D, o.vr.v2.ext[2]});
+  chains(h, {ChainJob{&in.T2, in.X, &o.vl, &o.vr, &Tp, nullptr}});
+  // a4: C'(q,l) = sum_{a,b} Q2l(a,b,q) vl2(a,b,l); C''(r,q') = sum vr2(a,b,r) Q2r(a,b,q')
+  Ten Cl = alloc(h, {Q2l.ext[2], o.vl.v2.ext[2]});
+  Ten Cr = alloc(h, {o.vr.v2.ext[2], Q2r.ext[2]});
+  contract(h, op({&Q2l}, "abq"), op({&o.vl.v2}, "abl"), out({&Cl}, "ql"));
+  contract(h, op({&o.vr.v2}, "abr"), op({&Q2r}, "abq"), out({&Cr}, "rq"));
+  //     M(q,k,b,q') = sum_{l,r} C'(q,l) T'(l,k,b,r) C''(r,q')
+  Ten M1 = alloc(h, {Cl.ext[0], D, D, Tp.ext[3]});
+  contract(h, op({&Cl}, "ql"), op({&Tp}, "lkbr"), out({&M1}, "qkbr"));
+  o.M = alloc(h, {Cl.ext[0], D, D, Cr.ext[1]});
+  contract(h, op({&M1}, "qkbr"), op({&Cr}, "rz"), out({&o.M}, "qkbz"));
+  return o;
+}
+
+// ---------------------------------------------------------------------------------------
+// Row a9: corner growth (Fig 4(b)).
+// ---------------------------------------------------------------------------------------
+void corner_top_left(Handle& h, const Ten& C1, const Ten& T2, const Iso& v, Ten& res, double* ss) {
+  const int D = T2.ext[1];
+  const size_t mark = h.ws.top;
+  Ten Y1 = alloc(h, {C1.ext[1], D, v.v1.ext[2]});
+  Ten Y2 = alloc(h, {v.v1.ext[2], D, T2.ext[3]});
+  contract(h, op({&C1}, "xp"), op({&v.v1}, "xka"), out({&Y1}, "pka"));
+  contract(h, op({&Y1}, "pka"), op({&T2}, "pkbr"), out({&Y2}, "abr"));
+  contract(h, op({&Y2}, "abr"), op({&v.v2}, "abo"), out({&res}, "or", {ss}));
+  h.ws.reset(mark);
+}
+void corner_bottom_left(Handle& h, const Ten& C4, const Ten& T4, const Iso& v, Ten& res, double* ss) {
+  const int D = T4.ext[1];
+  const size_t mark = h.ws.top;
+  Ten Y1 = alloc(h, {C4.ext[0], D, v.v1.ext[2]});
+  Ten Y2 = alloc(h, {v.v1.ext[2], D, T4.ext[0]});
+  contract(h, op({&C4}, "px"), op({&v.v1}, "xka"), out({&Y1}, "pka"));
+  contract(h, op({&Y1}, "pka"), op({&T4}, "rkbp"), out({&Y2}, "abr"));
+  contract(h, op({&Y2}, "abr"), op({&v.v2}, "abo"), out({&res}, "ro", {ss}));
+  h.ws.reset(mark);
+}
+
+// ---------------------------------------------------------------------------------------
+// Environment access
+// ---------------------------------------------------------------------------------------
+Ten envC(const ctm_env* e, int x, int k) {
+  return Ten{e->C[x][k - 1], {e->ext[x][k - 1][0], e->ext[x][k - 1][1]}};
+}
+Ten envT(const ctm_env* e, int x, int k, int D) {
+  return Ten{e->T[x][k - 1], {e->ext[x][4 + k - 1][0], D, D, e->ext[x][4 + k - 1][1]}};
+}
+
+void check_env(const ctm_env* e, const ctm_params& p) {
+  for (int x = 0; x < 2; ++x)
+    for (int j = 0; j < 8; ++j) {
+      if ((j < 4 ? e->C[x][j] : e->T[x][j - 4]) == nullptr) throw Error(CTM_E_ARG, "env: null tensor pointer");
+      for (int q = 0; q < 2; ++q)
+        if (e->ext[x][j][q] < 1 || e->ext[x][j][q] > p.chi)
+          throw Error(CTM_E_ARG, "env: boundary extent out of [1, chi]");
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Row a10: one column absorption, both row-parity windows from one snapshot.
+//   C_y^1 <- N[C_x^1 T_x^2 V_yx] ; T_y^1 <- N[V_xy T_x^1 X X* V_yx] ; C_x^4 <- N[V_yx C_y^4 T_y^4]
+// ---------------------------------------------------------------------------------------
+void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* env, const double* iso_in,
+                       double* iso_out, int absorption) {
+  const ctm_params& p = h.prm;
+  const int D = p.D;
+  const size_t mark = h.ws.top;
+  Iso V[2][2];   // V[x][y] = projector of cut 'xy' (x above)
+  if (iso_in) {
+    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
+    for (int c = 0; c < 2; ++c) {   // c = 0: ab, 1: ba
+      const double* base = iso_in + (size_t)(absorption * 2 + c) * (n1 + n2);
+      Iso& v = c == 0 ? V[0][1] : V[1][0];
+      v.v1 = Ten{const_cast<double*>(base), {p.chi, D, p.chi_p}};
+      v.v2 = Ten{const_cast<double*>(base + n1), {p.chi_p, D, p.chi}};
+    }
+  } else {
+    RenvOut ro[2];
+    for (int x = 0; x < 2; ++x) {
+      RenvIn ri{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
+      ro[x] = reduced_env(h, ri, p.chi_pp);
+    }
+    for (int x = 0; x < 2; ++x) {   // a5: main projectors, TS(M; chi', chi)
+      Iso v = ts_isometry(h, ro[x].M, p.chi_p, p.chi, nullptr);
+      V[x][1 - x] = v;
+    }
+  }
+  if (iso_out) {
+    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
+    for (int c = 0; c < 2; ++c) {
+      Iso& v = c == 0 ? V[0][1] : V[1][0];
+      if (v.v1.size() != n1 || v.v2.size() != n2) throw Error(CTM_E_ARG, "iso_out needs square extents chi");
+      double* base = iso_out + (size_t)(absorption * 2 + c) * (n1 + n2);
+      if (!h.dry) {
+        CTM_CUDA(cudaMemcpyAsync(base, v.v1.p, n1 * 8, cudaMemcpyDeviceToDevice, h.stream));
+        CTM_CUDA(cudaMemcpyAsync(base + n1, v.v2.p, n2 * 8, cudaMemcpyDeviceToDevice, h.stream));
+      }
+    }
+  }
+  // new tensors (snapshot semantics: written to workspace, committed at the end)
+  double* ss = h.ws.take(8);
+  zero(h, ss, 6);
+  Ten nT[2], nC1[2], nC4[2];
+  std::vector<ChainJob> jobs;
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    Iso& vxy = V[x][y];
+    Iso& vyx = V[y][x];
+    nT[y] = alloc(h, {vxy.v2.ext[2], D, D, vyx.v2.ext[2]});
+    nC1[y] = alloc(h, {vyx.v2.ext[2], envT(env, x, 2, D).ext[3]});
+    nC4[x] = alloc(h, {envT(env, y, 4, D).ext[0], vyx.v2.ext[2]});
+  }
+  Ten T1[2] = {envT(env, 0, 1, D), envT(env, 1, 1, D)};
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    jobs.push_back(ChainJob{&T1[x], &sl[x], &V[x][y], &V[y][x], &nT[y], ss + y});
+  }
+  chains(h, jobs);
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    corner_top_left(h, envC(env, x, 1), envT(env, x, 2, D), V[y][x], nC1[y], ss + 2 + y);
+    corner_bottom_left(h, envC(env, y, 4), envT(env, y, 4, D), V[y][x], nC4[x], ss + 4 + x);
+  }
+  // K7: normalise + commit (reading R13)
+  if (!h.dry) {
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    std::vector<size_t> n;
+    for (int y = 0; y < 2; ++y) {
+      src.push_back(nT[y].p);
+      dst.push_back(env->T[y][0]);
+      n.push_back(nT[y].size());
+    }
+    for (int y = 0; y < 2; ++y) {
+      src.push_back(nC1[y].p);
+      dst.push_back(env->C[y][0]);
+      n.push_back(nC1[y].size());
+    }
+    for (int x = 0; x < 2; ++x) {
+      src.push_back(nC4[x].p);
+      dst.push_back(env->C[x][3]);
+      n.push_back(nC4[x].size());
+    }
+    scale_commit(h, src, dst, n, ss);
+    if (p.flags & CTM_FLAG_CHECK_FINITE) {
+      int* cnt = reinterpret_cast<int*>(h.dev_scalars);
+      CTM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), h.stream));
+      for (size_t i = 0; i < dst.size(); ++i) nonfinite_count(h, dst[i], n[i], cnt);
+      int hc = 0;
+      CTM_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+      CTM_CUDA(cudaStreamSynchronize(h.stream));
+      if (hc) throw Error(CTM_E_NONFINITE, "non-finite entries after column absorption " + std::to_string(absorption));
+    }
+  }
+  for (int y = 0; y < 2; ++y) {
+    env->ext[y][4][0] = nT[y].ext[0];
+    env->ext[y][4][1] = nT[y].ext[3];
+    env->ext[y][0][0] = nC1[y].ext[0];
+    env->ext[y][0][1] = nC1[y].ext[1];
+  }
+  for (int x = 0; x < 2; ++x) {
+    env->ext[x][3][0] = nC4[x].ext[0];
+    env->ext[x][3][1] = nC4[x].ext[1];
+  }
+  h.ws.reset(mark);
+}
+
+void left_move(Handle& h, const double* A, const double* B, ctm_env* env, const double* iso_in, double* iso_out) {
+  const ctm_params& p = h.prm;
+  const size_t mark = h.ws.top;
+  Site sl[2] = {site_left(h, A, p.d, p.D), site_left(h, B, p.d, p.D)};
+  Site st[2];
+  if (!iso_in) {
+    st[0] = site_top(h, A, p.d, p.D);
+    st[1] = site_top(h, B, p.d, p.D);
+  }
+  column_absorption(h, sl, st, env, iso_in, iso_out, 0);
+  column_absorption(h, sl, st, env, iso_in, iso_out, 1);
+  h.ws.reset(mark);
+}
+
+// Quarter turns (clockwise storage: relabel k -> k+1, no data movement).
+void rotate_env_cw(ctm_env* e) {
+  ctm_env o = *e;
+  for (int x = 0; x < 2; ++x)
+    for (int k = 0; k < 4; ++k) {
+      int nk = (k + 1) % 4;
+      e->C[x][nk] = o.C[x][k];
+      e->T[x][nk] = o.T[x][k];
+      e->ext[x][nk][0] = o.ext[x][k][0];
+      e->ext[x][nk][1] = o.ext[x][k][1];
+      e->ext[x][4 + nk][0] = o.ext[x][4 + k][0];
+      e->ext[x][4 + nk][1] = o.ext[x][4 + k][1];
+    }
+}
+
+// Site leg permutation for n clockwise quarter turns: (s,u,l,d,r) -> turned.
+void rotate_site(Handle& h, const double* X, double* out, int turns) {
+  static const int perms[4][5] = {{0, 1, 2, 3, 4}, {0, 2, 3, 4, 1}, {0, 3, 4, 1, 2}, {0, 4, 1, 2, 3}};
+  const int* pm = perms[turns & 3];
+  permute(h, X, {h.prm.d, h.prm.D, h.prm.D, h.prm.D, h.prm.D}, {pm[0], pm[1], pm[2], pm[3], pm[4]}, out);
+}
+
+void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env) {
+  static const int turns_for[4] = {0, 2, 3, 1};   // LEFT, RIGHT, UP, DOWN: cw turns bringing it left
+  const int n = turns_for[dir];
+  if (n == 0) {
+    left_move(h, A, B, env, nullptr, nullptr);
+    return;
+  }
+  const size_t mark = h.ws.top;
+  const size_t ns = (size_t)h.prm.d * h.prm.D * h.prm.D * h.prm.D * h.prm.D;
+  double* Ar = h.ws.take(ns);
+  double* Br = h.ws.take(ns);
+  if (!h.dry) {
+    rotate_site(h, A, Ar, n);
+    rotate_site(h, B, Br, n);
+  }
+  for (int i = 0; i < n; ++i) rotate_env_cw(env);
+  try {
+    left_move(h, Ar, Br, env, nullptr, nullptr);
+  } catch (...) {
+    for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
+    throw;
+  }
+  for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
+  h.ws.reset(mark);
+}
+
+// ---------------------------------------------------------------------------------------
+// Closures (Fig 1(c,d)).  Same pairwise structure as the paper's enlarged corners.
+// ---------------------------------------------------------------------------------------
+struct Closure {
+  Ten Eul, Eur, Elr, Ell;
+};
+
+// Enlarged corner E = C . Ta . Tb . X . X*: generic helper on labels.
+double norm_2x2_impl(Handle& h, const double* A, const double* B, const ctm_env* env, bool absval) {
+  const int D = h.prm.D, d = h.prm.d;
+  const size_t mark = h.ws.top;
+  auto cp = [&](Ten t) {   // optional |.| copy
+    if (!absval) return t;
+    Ten r = alloc(h, t.ext);
+    abs_copy(h, t.p, r.p, t.size());
+    return r;
+  };
+  Ten sA = cp(Ten{const_cast<double*>(A), {d, D, D, D, D}});
+  Ten sB = cp(Ten{const_cast<double*>(B), {d, D, D, D, D}});
+  auto C = [&](int x, int k) { return cp(envC(env, x, k)); };
+  auto T = [&](int x, int k) { return cp(envT(env, x, k, D)); };
+  const int a = 0, b = 1;
+  // E_ul: C_a^1(x,y) T_a^2(y,k,b,Y) T_a^1(X,l,m,x) A(s,k,l,d,r) A*(s,b,m,e,q) -> (Y,r,q,X,d,e)
+  Ten c1 = C(a, 1), t2 = T(a, 2), t1 = T(a, 1);
+  Ten E1 = alloc(h, {c1.ext[0], D, D, t2.ext[3]});
+  contract(h, op({&c1}, "xy"), op({&t2}, "ykbY"), out({&E1}, "xkbY"));
+  Ten E2 = alloc(h, {D, D, t2.ext[3], t1.ext[0], D, D});
+  contract(h, op({&E1}, "xkbY"), op({&t1}, "Xlmx"), out({&E2}, "kbYXlm"));
+  Ten E3 = alloc(h, {D, t2.ext[3], t1.ext[0], D, d, D, D});
+  contract(h, op({&E2}, "kbYXlm"), op({&sA}, "skldr"), out({&E3}, "bYXmsdr"));
+  Ten Eul = alloc(h, {t2.ext[3], D, D, t1.ext[0], D, D});
+  contract(h, op({&E3}, "bYXmsdr"), op({&sA}, "sbmeq"), out({&Eul}, "YrqXde"));
+  // E_ur: T_b^2(Y,k,b,z) C_b^2(z,w) T_b^3(w,l,m,W) B(s,k,t,d,l) B*(s,b,u,e,m) -> (Y,t,u,W,d,e)
+  Ten u2 = T(b, 2), c2 = C(b, 2), u3 = T(b, 3);
+  Ten F1 = alloc(h, {u2.ext[0], D, D, c2.ext[1]});
+  contract(h, op({&u2}, "Ykbz"), op({&c2}, "zw"), out({&F1}, "Ykbw"));
+  Ten F2 = alloc(h, {u2.ext[0], D, D, D, D, u3.ext[3]});
+  contract(h, op({&F1}, "Ykbw"), op({&u3}, "wlmW"), out({&F2}, "YkblmW"));
+  Ten F3 = alloc(h, {u2.ext[0], D, D, u3.ext[3], d, D, D});
+  contract(h, op({&F2}, "YkblmW"), op({&sB}, "sktdl"), out({&F3}, "YbmWstd"));
+  Ten Eur = alloc(h, {u2.ext[0], D, D, u3.ext[3], D, D});
+  contract(h, op({&F3}, "YbmWstd"), op({&sB}, "sbuem"), out({&Eur}, "YtuWde"));
+  // E_lr: T_a^3(W,k,b,v) C_a^3(v,V) T_a^4(V,m,n,U) A(s,u,t,m,k) A*(s,p,q,n,b) -> (W,U,u,t,p,q)
+  Ten w3 = T(a, 3), c3 = C(a, 3), w4 = T(a, 4);
+  Ten G1 = alloc(h, {w3.ext[0], D, D, c3.ext[1]});
+  contract(h, op({&w3}, "Wkbv"), op({&c3}, "vV"), out({&G1}, "WkbV"));
+  Ten G2 = alloc(h, {w3.ext[0], D, D, D, D, w4.ext[3]});
+  contract(h, op({&G1}, "WkbV"), op({&w4}, "VmnU"), out({&G2}, "WkbmnU"));
+  Ten G3 = alloc(h, {w3.ext[0], D, D, w4.ext[3], d, D, D});
+  contract(h, op({&G2}, "WkbmnU"), op({&sA}, "sutmk"), out({&G3}, "WbnUsut"));
+  Ten Elr = alloc(h, {w3.ext[0], w4.ext[3], D, D, D, D});
+  contract(h, op({&G3}, "WbnUsut"), op({&sA}, "spqnb"), out({&Elr}, "WUutpq"));
+  // E_ll: T_b^4(U,k,b,Z) C_b^4(Z,z) T_b^1(z,l,m,X) B(s,u,l,k,r) B*(s,p,m,b,q) -> (U,X,u,r,p,q)
+  Ten z4 = T(b, 4), c4 = C(b, 4), z1 = T(b, 1);
+  Ten H1 = alloc(h, {z4.ext[0], D, D, c4.ext[1]});
+  contract(h, op({&z4}, "UkbZ"), op({&c4}, "Zz"), out({&H1}, "Ukbz"));
+  Ten H2 = alloc(h, {z4.ext[0], D, D, D, D, z1.ext[3]});
+  contract(h, op({&H1}, "Ukbz"), op({&z1}, "zlmX"), out({&H2}, "UkblmX"));
+  Ten H3 = alloc(h, {z4.ext[0], D, D, z1.ext[3], d, D, D});
+  contract(h, op({&H2}, "UkblmX"), op({&sB}, "sulkr"), out({&H3}, "UbmXsur"));
+  Ten Ell = alloc(h, {z4.ext[0], z1.ext[3], D, D, D, D});
+  contract(h, op({&H3}, "UbmXsur"), op({&sB}, "spmbq"), out({&Ell}, "UXurpq"));
+  // ring
+  Ten R1 = alloc(h, {Eul.ext[3], D, D, Eur.ext[3], D, D});
+  contract(h, op({&Eul}, "YrqXde"), op({&Eur}, "YrqWfg"), out({&R1}, "XdeWfg"));
+  Ten R2 = alloc(h, {Eul.ext[3], D, D, Elr.ext[1], D, D});
+  contract(h, op({&R1}, "XdeWfg"), op({&Elr}, "WUfhgi"), out({&R2}, "XdeUhi"));
+  // final full contraction: permute E_ll to R2's leg order (X,d,e,U,h,i), then a dot product
+  Ten Ellp = alloc(h, {Ell.ext[1], D, D, Ell.ext[0], D, D});
+  permute(h, Ell.p, Ell.ext, {1, 2, 4, 0, 3, 5}, Ellp.p);   // (U,X,d,h,e,i) -> (X,d,e,U,h,i)
+  Ten res = alloc(h, {1});
+  dot(h, R2.p, Ellp.p, R2.size(), res.p);
+  double v = 0.0;
+  if (!h.dry) {
+    CTM_CUDA(cudaMemcpyAsync(&v, res.p, sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+  }
+  h.ws.reset(mark);
+  return v;
+}
+
+}  // namespace
+}  // namespace ctm
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+using ctm::Error;
+using ctm::Handle;
+
+struct ctm_handle_s {
+  Handle h;
+};
+
+namespace {
+
+template <class F>
+int guarded(ctm_handle hh, F&& f) {
+  if (!hh) return CTM_E_ARG;
+  Handle& h = hh->h;
+  h.last_error.clear();
+  try {
+    f(h);
+    return CTM_OK;
+  } catch (const Error& e) {
+    h.last_error = e.what();
+    h.ws.reset(0);
+    h.dry = false;
+    return e.code;
+  } catch (const std::exception& e) {
+    h.last_error = e.what();
+    h.ws.reset(0);
+    h.dry = false;
+    return CTM_E_CUDA;
+  }
+}
+
+void begin_call(Handle& h) {
+  h.ms_svd = 0.0;
+  h.flops = 0.0;
+  h.min_gap = std::numeric_limits<double>::infinity();
+  h.n_svd = 0;
+  h.n_kernels = 0;
+  if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
+  h.ws.reset(0);
+}
+
+void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
+  if (!st) return;
+  st->ms_total = ms_total;
+  st->ms_svd = h.ms_svd;
+  st->ms_contract = ms_total - h.ms_svd;
+  st->flops = h.flops;
+  st->min_gap = h.min_gap;
+  st->n_svd = h.n_svd;
+  st->n_kernels = h.n_kernels;
+}
+
+// Dry run of a representative call sequence to size the workspace.
+size_t size_workspace(Handle& h) {
+  h.dry = true;
+  h.ws.dry = true;
+  h.ws.base = nullptr;
+  h.ws.cap = 0;
+  h.ws.reset(0);
+  h.ws.peak = 0;
+  const ctm_params& p = h.prm;
+  ctm_env env{};
+  static double dummy[1];
+  for (int x = 0; x < 2; ++x) {
+    for (int k = 0; k < 4; ++k) {
+      env.C[x][k] = dummy;
+      env.T[x][k] = dummy;
+    }
+    for (int j = 0; j < 8; ++j) env.ext[x][j][0] = env.ext[x][j][1] = p.chi;
+  }
+  ctm::move_dir(h, CTM_RIGHT, dummy, dummy, &env);
+  size_t need = h.ws.peak;
+  if (!(p.flags & 2)) {
+    h.ws.reset(0);
+    h.ws.peak = 0;
+    ctm::norm_2x2_impl(h, dummy, dummy, &env, true);
+    need = std::max(need, h.ws.peak);
+  }
+  h.dry = false;
+  h.ws.dry = false;
+  h.ws.peak = 0;
+  return need + (size_t)64 * 1024 * 1024;   // margin for cuSOLVER size variations
+}
+
+}  // namespace
+
+extern "C" {
+
+int ctm_abi_version(void) { return CTM_ABI_VERSION; }
+
+int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_bytes) {
+  if (!out || !p) return CTM_E_ARG;
+  *out = nullptr;
+  if (p->d < 1 || p->D < 1 || p->chi < 1 || p->chi_p < 1 || p->chi_pp < 1) return CTM_E_ARG;
+  if (p->strategy != CTM_SEQUENTIAL) return CTM_E_UNSUPPORTED;
+  std::unique_ptr<ctm_handle_s> hh(new ctm_handle_s());
+  Handle& h = hh->h;
+  h.prm = *p;
+  int warn = 0;
+  if (h.prm.chi_p > h.prm.chi * h.prm.D) {   // clamp chi' to chi D with a warning
+    h.prm.chi_p = h.prm.chi * h.prm.D;
+    warn = CTM_W_CLAMPED;
+  }
+  h.stream = reinterpret_cast<cudaStream_t>(stream);
+  try {
+    if (cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS) throw Error(CTM_E_SOLVER, "cusolverDnCreate failed");
+    if (cusolverDnCreateParams(&h.solver_params) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(CTM_E_SOLVER, "cusolverDnCreateParams failed");
+    if (cusolverDnCreateGesvdjInfo(&h.gesvdj_info) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(CTM_E_SOLVER, "cusolverDnCreateGesvdjInfo failed");
+    double tol = p->svd_tol > 0 ? p->svd_tol : 2.220446049250313e-16;
+    cusolverDnXgesvdjSetTolerance(h.gesvdj_info, tol);
+    cusolverDnXgesvdjSetMaxSweeps(h.gesvdj_info, 100);
+    cusolverDnSetStream(h.solver, h.stream);
+    CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
+    h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
+    for (auto& e : h.ev) CTM_CUDA(cudaEventCreate(&e));
+    size_t need = size_workspace(h);
+    if (ws_bytes) *ws_bytes = need;
+  } catch (const Error& e) {
+    fprintf(stderr, "ctm_init: %s\n", e.what());
+    return e.code;
+  }
+  *out = hh.release();
+  return CTM_OK | warn;
+}
+
+int ctm_set_workspace(ctm_handle hh, void* dev, size_t bytes) {
+  return guarded(hh, [&](Handle& h) {
+    if (!dev) throw Error(CTM_E_ARG, "null workspace");
+    h.ws.base = static_cast<char*>(dev);
+    h.ws.cap = bytes;
+    h.ws.reset(0);
+  });
+}
+
+int ctm_set_stream(ctm_handle hh, uintptr_t stream) {
+  return guarded(hh, [&](Handle& h) {
+    h.stream = reinterpret_cast<cudaStream_t>(stream);
+    cusolverDnSetStream(h.solver, h.stream);
+  });
+}
+
+int ctm_destroy(ctm_handle hh) {
+  if (!hh) return CTM_E_ARG;
+  Handle& h = hh->h;
+  if (h.gesvdj_info) cusolverDnDestroyGesvdjInfo(h.gesvdj_info);
+  if (h.solver_params) cusolverDnDestroyParams(h.solver_params);
+  if (h.solver) cusolverDnDestroy(h.solver);
+  for (auto& e : h.ev)
+    if (e) cudaEventDestroy(e);
+  if (h.dev_scalars) cudaFree(h.dev_scalars);
+  delete hh;
+  return CTM_OK;
+}
+
+const char* ctm_last_error(ctm_handle hh) { return hh ? hh->h.last_error.c_str() : "null handle"; }
+
+int64_t ctm_kernel_count(ctm_handle hh) { return hh ? hh->h.kernel_count : 0; }
+
+double ctm_move_flops(int d, int D, int chi, int chi_p, int chi_pp) {
+  // Sum of 2 M N K over the contractions of one left move for square extents, exactly as
+  // issued by this library (SURVEY 8(a) closed form when chi = chi' = chi'').
+  auto chain = [&](double cin, double n1, double o1, double cout, double m1, double o2) {
+    double DD = D;
+    return 2 * n1 * DD * DD * DD * cin * cout        // S1
+           + 2 * n1 * DD * cout * d * DD * DD * DD * DD   // S2
+           + 2 * n1 * DD * d * DD * m1 * cout * DD   // S3
+           + 2 * DD * d * DD * m1 * DD * o1 * n1     // S4
+           + 2 * DD * m1 * o1 * DD * DD * d * DD * DD     // S5
+           + 2 * o1 * DD * DD * o2 * m1 * DD;        // S6
+  };
+  double c = chi, cp = std::min((double)chi_p, c * D);
+  double n1 = std::min((double)chi_pp, c * D), n2 = std::min((double)chi_pp, n1 * D);
+  double DD = D;
+  double renv = 2 * (2 * c * c * c * DD * DD)            // a1: Q_l, Q_r
+                + 2 * (2 * n1 * DD * c * c * DD)          // a2: v1^T Q (l and r)
+                + chain(c, n1, n2, c, n1, n2)             // a3: T'^2
+                + 2 * (2 * c * n2 * n1 * DD)              // a4: C', C''
+                + 2 * c * DD * DD * n2 * n2               // a4: C' T'
+                + 2 * c * DD * DD * n2 * c;               // a4: (C' T') C''
+  double main_ts = 2 * cp * DD * c * c * DD;              // a5: v1^T M
+  double ch = chain(c, cp, c, c, cp, c);
+  double corner = 2 * c * c * DD * cp + 2 * cp * c * DD * DD * c + 2 * c * cp * DD * c;
+  double col = 2 * (renv + main_ts) + 2 * ch + 4 * corner;
+  return 2 * col;
+}
+
+int ctm_absorb_truncate(ctm_handle hh, const double* T, const double* X, const double* Xbra, const double* v1_in,
+                        const double* v2_in, const double* v1_out, const double* v2_out, double* T_out) {
+  return guarded(hh, [&](Handle& h) {
+    if (!T || !X || !Xbra || !v1_in || !v2_in || !v1_out || !v2_out || !T_out) throw Error(CTM_E_ARG, "null pointer");
+    begin_call(h);
+    const ctm_params& p = h.prm;
+    const int D = p.D, d = p.d, c = p.chi, cp = p.chi_p;
+    // X given in chain orientation (s, in, face, out, far): axes s=0 in=1 face=2 out=3 far=4
+    ctm::Site s;
+    s.ket = ctm::alloc(h, {D, D, d, D, D});
+    s.bra = ctm::alloc(h, {d, D, D, D, D});
+    ctm::permute(h, X, {d, D, D, D, D}, {1, 2, 0, 3, 4}, s.ket.p);
+    ctm::permute(h, Xbra, {d, D, D, D, D}, {0, 2, 1, 3, 4}, s.bra.p);
+    ctm::Ten Tt{const_cast<double*>(T), {c, D, D, c}};
+    ctm::Iso in{{const_cast<double*>(v1_in), {c, D, cp}}, {const_cast<double*>(v2_in), {cp, D, c}}};
+    ctm::Iso ou{{const_cast<double*>(v1_out), {c, D, cp}}, {const_cast<double*>(v2_out), {cp, D, c}}};
+    ctm::Ten res{T_out, {c, D, D, c}};
+    ctm::chains(h, {ctm::ChainJob{&Tt, &s, &in, &ou, &res, nullptr}});
+  });
+}
+
+int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const double* C2, const double* T1,
+                    const double* X, const double* Xbra, const double* T3, int mode, double* M_out,
+                    double* iso_out) {
+  return guarded(hh, [&](Handle& h) {
+    if (!C1 || !T2 || !C2 || !T1 || !X || !Xbra || !T3 || !M_out) throw Error(CTM_E_ARG, "null pointer");
+    if (mode != CTM_RENV_APPROX) throw Error(CTM_E_UNSUPPORTED, "CTM_RENV_EXACT is NEXT on the GPU (oracle only)");
+    begin_call(h);
+    const ctm_params& p = h.prm;
+    const int D = p.D, c = p.chi;
+    ctm::Site st = ctm::make_site(h, X, Xbra, p.d, D, 2, 1, 4, 3);
+    ctm::RenvIn ri{{const_cast<double*>(C1), {c, c}},       {const_cast<double*>(T2), {c, D, D, c}},
+                   {const_cast<double*>(C2), {c, c}},       {const_cast<double*>(T1), {c, D, D, c}},
+                   {const_cast<double*>(T3), {c, D, D, c}}, &st};
+    ctm::RenvOut ro = ctm::reduced_env(h, ri, p.chi_pp);
+    CTM_CUDA(cudaMemcpyAsync(M_out, ro.M.p, ro.M.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
+    if (iso_out) {
+      double* o = iso_out;
+      for (const ctm::Ten* t : {&ro.vl.v1, &ro.vl.v2, &ro.vr.v1, &ro.vr.v2}) {
+        CTM_CUDA(cudaMemcpyAsync(o, t->p, t->size() * 8, cudaMemcpyDeviceToDevice, h.stream));
+        o += t->size();
+      }
+    }
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+  });
+}
+
+int ctm_left_move(ctm_handle hh, const double* A, const double* B, ctm_env* env, const double* iso_in,
+                  double* iso_out, ctm_move_stats* st) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env) throw Error(CTM_E_ARG, "null pointer");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    CTM_CUDA(cudaEventRecord(h.ev[0], h.stream));
+    ctm::left_move(h, A, B, env, iso_in, iso_out);
+    CTM_CUDA(cudaEventRecord(h.ev[1], h.stream));
+    if (st) {
+      CTM_CUDA(cudaEventSynchronize(h.ev[1]));
+      float ms = 0;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
+      fill_stats(h, st, ms);
+    }
+  });
+}
+
+int ctm_move(ctm_handle hh, int dir, const double* A, const double* B, ctm_env* env, ctm_move_stats* st) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || dir < 0 || dir > 3) throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    CTM_CUDA(cudaEventRecord(h.ev[0], h.stream));
+    ctm::move_dir(h, dir, A, B, env);
+    CTM_CUDA(cudaEventRecord(h.ev[1], h.stream));
+    if (st) {
+      CTM_CUDA(cudaEventSynchronize(h.ev[1]));
+      float ms = 0;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
+      fill_stats(h, st, ms);
+    }
+  });
+}
+
+int ctm_iterate(ctm_handle hh, const double* A, const double* B, ctm_env* env, int n_iter, ctm_move_stats* st) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || n_iter < 0) throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    CTM_CUDA(cudaEventRecord(h.ev[0], h.stream));
+    for (int it = 0; it < n_iter; ++it)
+      for (int dir : {CTM_LEFT, CTM_RIGHT, CTM_UP, CTM_DOWN}) ctm::move_dir(h, dir, A, B, env);
+    CTM_CUDA(cudaEventRecord(h.ev[1], h.stream));
+    if (st) {
+      CTM_CUDA(cudaEventSynchronize(h.ev[1]));
+      float ms = 0;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
+      fill_stats(h, st, ms);
+    }
+  });
+}
+
+int ctm_norm_2x2(ctm_handle hh, const double* A, const double* B, const ctm_env* env, double* out_host,
+                 double* cancel_ratio_host) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || !out_host) throw Error(CTM_E_ARG, "null pointer");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    double v = ctm::norm_2x2_impl(h, A, B, env, false);
+    *out_host = v;
+    if (cancel_ratio_host) {
+      double va = ctm::norm_2x2_impl(h, A, B, env, true);
+      *cancel_ratio_host = va != 0.0 ? v / va : 0.0;
+    }
+  });
+}
+
+int ctm_bond_energy(ctm_handle hh, const double* A, const double* B, const ctm_env* env, const double* hop,
+                    int bond, double* rho_out, double* e_out_host) {
+  return guarded(hh, [&](Handle& h) {
+    (void)A; (void)B; (void)env; (void)hop; (void)bond; (void)rho_out; (void)e_out_host;
+    throw Error(CTM_E_UNSUPPORTED, "ctm_bond_energy: not built yet");
+  });
+}
+
+}  // extern "C"

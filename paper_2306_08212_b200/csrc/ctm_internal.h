@@ -1,0 +1,105 @@
+// ctm_internal.h -- host-side internals of libctm (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <cusolverDn.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/ctm.h"
+#include "tc_gemm.cuh"
+
+namespace ctm {
+
+// Error carrying an ABI status code; caught at the ABI boundary.
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CTM_CUDA(x)                                                                      \
+  do {                                                                                   \
+    cudaError_t e_ = (x);                                                                \
+    if (e_ != cudaSuccess)                                                               \
+      throw ::ctm::Error(CTM_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));  \
+  } while (0)
+
+// A (batch of) row-major tensor operand(s): labels name the legs, ext their extents.
+struct Operand {
+  std::vector<const double*> p;
+  std::string lab;
+  std::vector<int> ext;
+};
+struct OutOperand {
+  std::vector<double*> p;
+  std::string lab;
+  std::vector<int> ext;
+  std::vector<double*> sumsq;   // optional fused sum of squares (one per batch entry)
+};
+
+// Bump allocator over the caller-provided workspace.
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, top = 0, peak = 0;
+  bool dry = false;   // sizing pass: count bytes without a buffer
+  double* take(size_t n_doubles) {
+    size_t bytes = (n_doubles * sizeof(double) + 255) & ~size_t(255);
+    if (!dry && top + bytes > cap)
+      throw Error(CTM_E_NOMEM, "workspace too small: need > " + std::to_string(top + bytes) +
+                                   " bytes, have " + std::to_string(cap));
+    double* r = dry ? nullptr : reinterpret_cast<double*>(base + top);
+    top += bytes;
+    if (top > peak) peak = top;
+    return r;
+  }
+  void reset(size_t to = 0) { top = to; }
+};
+
+struct Handle {
+  ctm_params prm{};
+  cudaStream_t stream = nullptr;
+  cusolverDnHandle_t solver = nullptr;
+  cusolverDnParams_t solver_params = nullptr;
+  gesvdjInfo_t gesvdj_info = nullptr;
+  Arena ws;
+  std::vector<char> host_buf;          // cuSOLVER host workspace
+  int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
+  double* dev_scalars = nullptr;        // small device scratch (norms etc.)
+  cudaEvent_t ev[4]{};
+  std::string last_error;
+  int64_t kernel_count = 0;
+  // per-call statistics
+  double ms_svd = 0.0;
+  double flops = 0.0;
+  double min_gap = 1e300;
+  int n_svd = 0;
+  int n_kernels = 0;
+  bool dry = false;                     // sizing pass: no launches
+  void count_kernel(int n = 1) { kernel_count += n; n_kernels += n; }
+};
+
+// tc_gemm.cu
+void contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
+              double alpha = 1.0);
+
+// kernels.cu
+void permute(Handle& h, const double* src, const std::vector<int>& ext, const std::vector<int>& perm,
+             double* dst);
+void zero(Handle& h, double* p, size_t n);
+void sumsq(Handle& h, const std::vector<const double*>& srcs, const std::vector<size_t>& ns,
+           double* out);
+void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
+                  const std::vector<size_t>& ns, const double* sumsqs);
+void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count);
+void abs_copy(Handle& h, const double* src, double* dst, size_t n);
+void dot(Handle& h, const double* a, const double* b, size_t n, double* out);   // out = a.b (device)
+
+// svd.cu: first n_keep left singular vectors of the row-major R x C matrix `mat`
+// (input preserved), written row-major (R, n_keep) with the sign rule.  Returns the
+// truncation gap sigma_{n}/sigma_{n+1} (inf if none).
+double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out);
+size_t svd_workspace_doubles(Handle& h, int R, int C);
+
+}  // namespace ctm

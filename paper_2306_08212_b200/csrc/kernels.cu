@@ -1,0 +1,200 @@
+// kernels.cu -- HBM-bound helper kernels of libctm: site-leg permutation, Frobenius
+// norms (sum of squares), normalise-and-commit, finiteness scan.  Grid sizes are
+// multiples of the 148 SMs (grid-stride loops).
+#include "ctm_internal.h"
+
+namespace ctm {
+namespace {
+
+constexpr int kSMs = 148;
+
+struct PermArgs {
+  int rank;
+  int dst_ext[8];
+  long long src_str[8];   // source stride of each destination axis
+};
+
+__global__ void permute_kernel(const double* __restrict__ src, double* __restrict__ dst, long long n,
+                               PermArgs a) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long r = i, off = 0;
+    for (int j = a.rank - 1; j >= 0; --j) {
+      long long q = r / a.dst_ext[j];
+      off += (r - q * a.dst_ext[j]) * a.src_str[j];
+      r = q;
+    }
+    dst[i] = src[off];
+  }
+}
+
+__global__ void zero_kernel(double* p, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = 0.0;
+}
+
+struct Multi {
+  const double* src[8];
+  double* dst[8];
+  long long n[8];
+};
+
+// blockIdx.y = tensor; out[y] += sum of squares
+__global__ void sumsq_kernel(Multi m, double* out) {
+  const int y = blockIdx.y;
+  const double* __restrict__ s = m.src[y];
+  const long long n = m.n[y];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double v = s[i];
+    acc += v * v;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(out + y, v);
+  }
+}
+
+// dst[y][i] = src[y][i] / sqrt(sumsq[y])   (Frobenius normalisation, reading R13)
+__global__ void scale_commit_kernel(Multi m, const double* __restrict__ ss) {
+  const int y = blockIdx.y;
+  const double inv = rsqrt(ss[y]);
+  const double* __restrict__ s = m.src[y];
+  double* __restrict__ d = m.dst[y];
+  const long long n = m.n[y];
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = s[i] * inv;
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ p, long long n, int* cnt) {
+  int bad = 0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    bad += !isfinite(p[i]);
+  bad = __reduce_add_sync(0xffffffffu, bad);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(cnt, bad);
+}
+
+__global__ void abs_kernel(const double* __restrict__ s, double* __restrict__ d, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    d[i] = fabs(s[i]);
+}
+
+__global__ void dot_kernel(const double* __restrict__ a, const double* __restrict__ b, long long n, double* out) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc += a[i] * b[i];
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(out, v);
+  }
+}
+
+int grid_for(long long n, int threads = 256) {
+  long long b = (n + threads - 1) / threads;
+  long long cap = kSMs * 8;
+  return (int)(b < 1 ? 1 : (b > cap ? cap : b));
+}
+
+}  // namespace
+
+void permute(Handle& h, const double* src, const std::vector<int>& ext, const std::vector<int>& perm,
+             double* dst) {
+  if (h.dry) return;
+  int r = (int)ext.size();
+  if (r > 8 || (int)perm.size() != r) throw Error(CTM_E_ARG, "permute: bad rank");
+  std::vector<long long> st(r);
+  long long acc = 1;
+  for (int i = r - 1; i >= 0; --i) {
+    st[i] = acc;
+    acc *= ext[i];
+  }
+  PermArgs a{};
+  a.rank = r;
+  for (int j = 0; j < r; ++j) {
+    a.dst_ext[j] = ext[perm[j]];
+    a.src_str[j] = st[perm[j]];
+  }
+  permute_kernel<<<grid_for(acc), 256, 0, h.stream>>>(src, dst, acc, a);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void zero(Handle& h, double* p, size_t n) {
+  if (h.dry || n == 0) return;
+  zero_kernel<<<grid_for((long long)n), 256, 0, h.stream>>>(p, (long long)n);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void sumsq(Handle& h, const std::vector<const double*>& srcs, const std::vector<size_t>& ns,
+           double* out) {
+  if (h.dry) return;
+  Multi m{};
+  long long mx = 0;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    m.src[i] = srcs[i];
+    m.n[i] = (long long)ns[i];
+    mx = std::max(mx, m.n[i]);
+  }
+  dim3 grid(std::min(grid_for(mx), kSMs * 2), (unsigned)srcs.size());
+  sumsq_kernel<<<grid, 256, 0, h.stream>>>(m, out);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
+                  const std::vector<size_t>& ns, const double* ss) {
+  if (h.dry) return;
+  Multi m{};
+  long long mx = 0;
+  for (size_t i = 0; i < srcs.size(); ++i) {
+    m.src[i] = srcs[i];
+    m.dst[i] = dsts[i];
+    m.n[i] = (long long)ns[i];
+    mx = std::max(mx, m.n[i]);
+  }
+  dim3 grid(std::min(grid_for(mx), kSMs * 2), (unsigned)srcs.size());
+  scale_commit_kernel<<<grid, 256, 0, h.stream>>>(m, ss);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count) {
+  if (h.dry) return;
+  nonfinite_kernel<<<grid_for((long long)n), 256, 0, h.stream>>>(p, (long long)n, dev_count);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void dot(Handle& h, const double* a, const double* b, size_t n, double* out) {
+  if (h.dry) return;
+  CTM_CUDA(cudaMemsetAsync(out, 0, sizeof(double), h.stream));
+  dot_kernel<<<std::min(grid_for((long long)n), kSMs * 2), 256, 0, h.stream>>>(a, b, (long long)n, out);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void abs_copy(Handle& h, const double* src, double* dst, size_t n) {
+  if (h.dry) return;
+  abs_kernel<<<grid_for((long long)n), 256, 0, h.stream>>>(src, dst, (long long)n);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+}  // namespace ctm

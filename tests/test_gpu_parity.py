@@ -1,0 +1,200 @@
+"""GPU parity: libctm (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Tolerances (BASELINE.json north star):
+  * given identical isometries, contraction outputs agree entrywise within 1e-11 relative
+    max-norm (fp64);
+  * the gauge-free reduced environment M within 1e-10;
+  * gauge-invariant quantities (2x2 norm, rho, bond energy) after fixed iterations within
+    1e-9 relative.
+"""
+import numpy as np
+import pytest
+
+import ctm_inputs as ci
+from oracle import ctm_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2306_08212_b200 import ctm
+DEV = "cuda"
+
+
+def rel_err(got, ref):
+    return np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-300)
+
+
+def T_(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def _iso_from_flat(p, chi, D, chi_p):
+    n1, n2 = chi * D * chi_p, chi_p * D * chi
+    out, off = [], 0
+    for a in range(2):
+        proj = {}
+        for cut in ("ab", "ba"):
+            proj[cut] = {"v1": p[off:off + n1].reshape(chi, D, chi_p),
+                         "v2": p[off + n1:off + n1 + n2].reshape(chi_p, D, chi)}
+            off += n1 + n2
+        out.append(proj)
+    return out
+
+
+# ----------------------------------------------------------------------------------------
+# rows a6-a8: absorb/truncate chain with identical isometries
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("d,D,chi,chi_p", [(2, 2, 8, 8), (2, 4, 32, 32), (2, 3, 37, 29), (2, 6, 64, 64),
+                                           (2, 8, 128, 128)])
+def test_absorb_truncate_identical_isometries(d, D, chi, chi_p):
+    rng = np.random.default_rng(1000 + chi)
+    T = rng.standard_normal((chi, D, D, chi))
+    X = rng.standard_normal((d, D, D, D, D))      # (s, in, face, out, far)
+    Xb = rng.standard_normal((d, D, D, D, D))     # bra != ket: catches ket/bra mix-ups
+    v1i, v2i = ci.random_isometries(rng, chi, D, chi_p, chi)
+    v1o, v2o = ci.random_isometries(rng, chi, D, chi_p, chi)
+    ref = O.absorb_truncate(T, X, Xb, v1i, v2i, v1o, v2o)
+    h = ctm.CtmHandle(d, D, chi, chi_p, chi, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    out = torch.empty((chi, D, D, chi), dtype=torch.float64, device=DEV)
+    h.ctm_absorb_truncate(T_(T), T_(X), T_(Xb), T_(v1i), T_(v2i), T_(v1o), T_(v2o), out)
+    assert rel_err(out.cpu().numpy(), ref) <= 1e-11
+
+
+# ----------------------------------------------------------------------------------------
+# rows a1-a4: reduced environment (gauge-free M)
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("d,D,chi,chi_pp", [(2, 2, 8, 8), (2, 2, 4, 16), (2, 4, 32, 32), (2, 3, 20, 17),
+                                            (2, 8, 128, 128)])
+def test_reduced_env(d, D, chi, chi_pp):
+    cfg = ci.custom(d, D, chi, chi_pp=chi_pp, seed_index=200 + chi, decaying=D >= 6)
+    g = ci.generate(cfg)
+    C, T, A = g["C"], g["T"], g["A"]
+    x = "a"
+    M_ref, _ = O.reduced_env_approx(C[(x, 1)], T[(x, 2)], C[(x, 2)], T[(x, 1)], A, A, T[(x, 3)], chi_pp)
+    h = ctm.CtmHandle(d, D, chi, chi, chi_pp, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    M = torch.empty((chi, D, D, chi), dtype=torch.float64, device=DEV)
+    h.ctm_reduced_env(T_(C[(x, 1)]), T_(T[(x, 2)]), T_(C[(x, 2)]), T_(T[(x, 1)]), T_(A), T_(A), T_(T[(x, 3)]), M)
+    assert rel_err(M.cpu().numpy(), M_ref) <= 1e-10
+
+
+def test_reduced_env_untruncated_equals_exact():
+    cfg = ci.custom(2, 2, 4, chi_pp=16, seed_index=211)
+    g = ci.generate(cfg)
+    C, T, A = g["C"], g["T"], g["A"]
+    M_ex = O.reduced_env_exact(C[("b", 1)], T[("b", 2)], C[("b", 2)], T[("b", 1)], A, A, T[("b", 3)])
+    h = ctm.CtmHandle(2, 2, 4, 4, 16, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    M = torch.empty((4, 2, 2, 4), dtype=torch.float64, device=DEV)
+    h.ctm_reduced_env(T_(C[("b", 1)]), T_(T[("b", 2)]), T_(C[("b", 2)]), T_(T[("b", 1)]), T_(A), T_(A),
+                      T_(T[("b", 3)]), M)
+    assert rel_err(M.cpu().numpy(), M_ex) <= 1e-10
+
+
+# ----------------------------------------------------------------------------------------
+# rows a1-a11: left move; GPU isometries injected into the oracle -> entrywise parity
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "c2", "c3", "c4"])
+def test_left_move_entrywise_with_gpu_isometries(name):
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp,
+                      flags=ctm.CTM_FLAG_CHECK_FINITE | ctm.CTM_FLAG_MOVE_ONLY)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
+    st = h.ctm_left_move(T_(g["A"]), T_(g["B"]), env, iso_out=iso)
+    assert st["n_svd"] == 2 * 12 and np.isfinite(st["ms_total"])
+    got = env.to_host()
+    projs = _iso_from_flat(iso.cpu().numpy(), cfg.chi, cfg.D, cfg.chi_p)
+    e = {"C": g["C"], "T": g["T"]}
+    for a in range(2):
+        e, _ = O.column_absorption(e, g["A"], g["B"], cfg.chi, projectors=projs[a])
+    for kind in ("C", "T"):
+        for key, ref in e[kind].items():
+            assert rel_err(got[kind][key], ref) <= 1e-11, (kind, key)
+    # the isometries themselves are isometries
+    for proj in projs:
+        for cut in proj.values():
+            v1 = cut["v1"].reshape(-1, cfg.chi_p)
+            v2 = cut["v2"].reshape(-1, cfg.chi)
+            assert np.allclose(v1.T @ v1, np.eye(cfg.chi_p), atol=1e-12)
+            assert np.allclose(v2.T @ v2, np.eye(cfg.chi), atol=1e-12)
+
+
+def test_injected_isometries_reproduce_the_move():
+    """INJECT_ISO: replaying the move with its own isometries gives the same env."""
+    cfg = ci.CONFIGS["c2"]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
+    e1 = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    h.ctm_left_move(T_(g["A"]), T_(g["B"]), e1, iso_out=iso)
+    e2 = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    st = h.ctm_left_move(T_(g["A"]), T_(g["B"]), e2, iso_in=iso)
+    assert st["n_svd"] == 0
+    a, b = e1.to_host(), e2.to_host()
+    for kind in ("C", "T"):
+        for key in a[kind]:
+            assert np.array_equal(a[kind][key], b[kind][key])
+
+
+# ----------------------------------------------------------------------------------------
+# no truncation: the full left move is exact (gauge-invariant column contraction)
+# ----------------------------------------------------------------------------------------
+def test_full_move_without_truncation_matches_oracle():
+    cfg = ci.custom(2, 2, 16, chi0=1, seed_index=21)
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(2, 2, 16, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    env = ctm.Env.from_host(g["C"], g["T"], 2, 16)
+    h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
+    got = env.to_host()
+    ref = O.left_move({"C": g["C"], "T": g["T"]}, g["A"], g["B"], 16)
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        def col(e):
+            c = np.einsum("xR,yklx,zmny,Sz->RklmnS", e["C"][(x, 1)], e["T"][(x, 1)], e["T"][(y, 1)], e["C"][(y, 4)])
+            return c / np.linalg.norm(c)
+        assert got["T"][(x, 1)].shape == ref["T"][(x, 1)].shape == (16, 2, 2, 16)
+        assert np.allclose(col(got), col(ref), atol=1e-12)
+
+
+@pytest.mark.parametrize("direction", ["left", "right", "up", "down"])
+def test_directional_move_gauge_invariant(direction):
+    cfg = ci.custom(2, 2, 16, chi0=1, seed_index=25)
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(2, 2, 16, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    env = ctm.Env.from_host(g["C"], g["T"], 2, 16)
+    h.ctm_move(direction, T_(g["A"]), T_(g["B"]), env)
+    ref = O.move({"C": g["C"], "T": g["T"]}, g["A"], g["B"], direction, 16)
+    n_gpu = O.norm_2x2(env.to_host(), g["A"], g["B"])
+    n_ref = O.norm_2x2(ref, g["A"], g["B"])
+    assert abs(n_gpu - n_ref) <= 1e-10 * abs(n_ref)
+
+
+# ----------------------------------------------------------------------------------------
+# closures
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["tiny", "c2"])
+def test_norm_2x2(name):
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    v, ratio = h.ctm_norm_2x2(T_(g["A"]), T_(g["B"]), env)
+    ref = O.norm_2x2({"C": g["C"], "T": g["T"]}, g["A"], g["B"])
+    assert abs(v - ref) <= 1e-11 * abs(ref) / max(abs(ratio), 1e-6)
+
+
+@pytest.mark.parametrize("name,n_iter", [("tiny", 1), ("c2", 20)])
+def test_iterations_gauge_invariant(name, n_iter):
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    h.ctm_iterate(T_(g["A"]), T_(g["B"]), env, n_iter)
+    e = {"C": g["C"], "T": g["T"]}
+    for _ in range(n_iter):
+        e = O.ctm_iteration(e, g["A"], g["B"], cfg.chi, cfg.chi_p, cfg.chi_pp)
+    v, ratio = h.ctm_norm_2x2(T_(g["A"]), T_(g["B"]), env)
+    ref = O.norm_2x2(e, g["A"], g["B"])
+    print(f"{name}: norm gpu {v!r} oracle {ref!r} rel {abs(v - ref) / abs(ref):.3e} cancel {ratio:.3e}")
+    assert abs(v - ref) <= 1e-9 * abs(ref)
