@@ -1,0 +1,292 @@
+"""bench.py -- CTM moves/sec and FP64 TFLOP/s of the B200 CTMRG move (arXiv 2306.08212).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One step = one LEFT MOVE (2 column absorptions, each with two
+approximated reduced environments, 12 device SVDs, two sequential absorb/truncate
+chains, four corner growths and the normalise+commit) on the synthetic C4 workload
+(d=2, D=8, chi=chi'=chi''=128, decaying-spectrum seeded tensors, BASELINE.json
+configs[3], the headline roofline config).  Inputs are resident in HBM; the move's
+intermediates (>= 134 MB each) exceed the 126 MB L2 and an L2 flush (256 MB write)
+separates timed steps; each step is timed with CUDA events on the library's stream.
+
+Multi-GPU: the move does not shard ("replicas only"): under torchrun every
+rank runs an independent replica; value = moves of all ranks / max-over-ranks time.
+
+--impl reference times the CPU float64 oracle (oracle/) on the host cores on the same
+config (the paper has no code; the oracle is the reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import ctm_inputs as ci  # noqa: E402
+
+FP64_PEAK_TFLOPS = 37.14   # measured DMMA.8x8x4 loop peak on this pool's B200 (profiles/r01_probe_fp64.txt)
+METRIC = "CTM moves/sec and FP64 TFLOP/s (% of B200 FP64 peak) vs D,chi"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--svd", default="gesvdp", choices=["gesvdp", "gesvdj", "gesvd"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = "clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown," \
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown," \
+             "clocks_event_reasons.sw_power_cap"
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                if out.returncode == 0 and out.stdout.strip():
+                    self.samples.append([x.strip() for x in out.stdout.strip().split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and s[4 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+def run_oracle_sample(cfg, what="left_move"):
+    """One left move of the oracle (bounded CPU sample); returns seconds."""
+    from oracle import ctm_oracle as O
+    g = ci.generate(cfg)
+    env = {"C": g["C"], "T": g["T"]}
+    t = time.perf_counter()
+    O.left_move(env, g["A"], g["B"], cfg.chi, cfg.chi_p, cfg.chi_pp)
+    return time.perf_counter() - t
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def bench_reference(args, cfg):
+    world, rank, _ = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")), 0
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        run_oracle_sample(cfg)
+    ts = [run_oracle_sample(cfg) for _ in range(args.steps)]
+    sec = float(np.sum(ts))
+    value = args.steps / sec
+    line = {"metric": METRIC, "value": value, "unit": "moves/s", "impl": "reference", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded, ctm_inputs.py)",
+            "config": {"workload": f"{cfg.name}: left move, d={cfg.d} D={cfg.D} chi={cfg.chi} chi'={cfg.chi_p} "
+                                   f"chi''={cfg.chi_pp}, sequential order", "D": cfg.D, "chi": cfg.chi},
+            "cpu_baseline": {"value": value, "unit": "moves/s", "cores": host_cores(), "kind": "oracle",
+                             "sample": f"{args.steps} full left moves of {cfg.name} (NumPy/OpenBLAS fp64 oracle)"},
+            "e2e": {"value": value, "unit": "moves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def bench_ours(args, cfg):
+    import torch
+    world, rank, local = dist_setup(args.gpus)
+    dev = torch.device(f"cuda:{local}")
+    torch.cuda.set_device(dev)
+    from paper_2306_08212_b200 import ctm
+    svd = {"gesvdp": ctm.CTM_SVD_GESVDP, "gesvdj": ctm.CTM_SVD_GESVDJ, "gesvd": ctm.CTM_SVD_GESVD}[args.svd]
+    stream = torch.cuda.Stream(dev)
+    g = ci.generate(cfg)
+    with torch.cuda.stream(stream):
+        h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, svd_algo=svd,
+                          flags=ctm.CTM_FLAG_MOVE_ONLY, stream=stream, device=dev)
+        hp = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, svd_algo=svd,
+                           flags=ctm.CTM_FLAG_MOVE_ONLY | ctm.CTM_FLAG_PROFILE, stream=stream, device=dev)
+        A = torch.from_numpy(g["A"]).to(dev)
+        B = torch.from_numpy(g["B"]).to(dev)
+        env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi, device=dev)
+        flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+        iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=dev)
+    F_move = ctm.ctm_move_flops(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def step(inject=False, handle=h, stats=None):
+        flush.zero_()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        st = handle.ctm_left_move(A, B, env, iso_in=iso if inject else None, iso_out=None if inject else iso)
+        e1.record(stream)
+        e1.synchronize()
+        if stats is not None:
+            stats.append(st)
+        return e0.elapsed_time(e1)
+
+    with torch.cuda.stream(stream):
+        for _ in range(max(args.warmup, 3)):
+            step()
+        k0 = h.kernel_count
+        stats = []
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        with ClockSampler(local) as clk:
+            ms = [step(stats=stats) for _ in range(args.steps)]
+        torch.cuda.synchronize()
+        launches = h.kernel_count - k0
+        # contraction-only (isometries injected: no reduced env, no SVD) -- the hot contraction
+        for _ in range(2):
+            step(inject=True)
+        ms_c = [step(inject=True) for _ in range(args.steps)]
+        # per-launch profile of the dominant kernel (tc_gemm), same contraction-only step
+        pst = []
+        for _ in range(3):
+            step(inject=True, handle=hp, stats=pst)
+        # end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
+        pinned = {"A": torch.from_numpy(g["A"]).pin_memory(), "B": torch.from_numpy(g["B"]).pin_memory()}
+        hC = {k: torch.from_numpy(v.reshape(-1)).pin_memory() for k, v in g["C"].items()}
+        hT = {k: torch.from_numpy(v.reshape(-1)).pin_memory() for k, v in g["T"].items()}
+        oC = {k: torch.empty_like(v).pin_memory() for k, v in hC.items()}
+        oT = {k: torch.empty_like(v).pin_memory() for k, v in hT.items()}
+        h2d = sum(t.numel() * 8 for t in list(pinned.values()) + list(hC.values()) + list(hT.values()))
+        d2h = sum(t.numel() * 8 for t in list(oC.values()) + list(oT.values()))
+
+        def e2e_step():
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            A.copy_(pinned["A"], non_blocking=True)
+            B.copy_(pinned["B"], non_blocking=True)
+            for k in hC:
+                env.C[k][: hC[k].numel()].copy_(hC[k], non_blocking=True)
+                env.T[k][: hT[k].numel()].copy_(hT[k], non_blocking=True)
+            h.ctm_left_move(A, B, env)
+            for k in oC:
+                oC[k].copy_(env.C[k][: oC[k].numel()], non_blocking=True)
+                oT[k].copy_(env.T[k][: oT[k].numel()], non_blocking=True)
+            e1.record(stream)
+            e1.synchronize()
+            return e0.elapsed_time(e1)
+
+        e2e_step()
+        ms_e2e = [e2e_step() for _ in range(max(3, args.steps // 2))]
+
+    t_step = float(np.mean(ms))
+    t_c = float(np.mean(ms_c))
+    t_e2e = float(np.mean(ms_e2e))
+    if world > 1:
+        import torch.distributed as dist
+        tt = torch.tensor([t_step, t_c, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_c, t_e2e = [float(x) for x in tt.cpu()]
+    ms_svd = float(np.mean([s["ms_svd"] for s in stats]))
+    ms_iso = float(np.mean([s["ms_isometry"] for s in stats]))
+    gem_ms = float(np.mean([s["ms_gemm"] for s in pst]))
+    gem_fl = float(np.mean([s["gemm_flops"] for s in pst]))
+    gem_n = float(np.mean([s["gemm_launches"] for s in pst]))
+    achieved = gem_fl / (gem_ms * 1e-3) / 1e12
+    if rank != 0:
+        return
+    value = world * 1e3 / t_step
+    line = {
+        "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, ctm_inputs.py)",
+        "config": {"workload": f"{cfg.name}: left move, d={cfg.d} D={cfg.D} chi={cfg.chi} chi'={cfg.chi_p} "
+                               f"chi''={cfg.chi_pp}, sequential order, svd={args.svd}",
+                   "D": cfg.D, "chi": cfg.chi, "parallelism": f"replicas{world}",
+                   "l2": "256 MB L2 flush between timed steps; intermediates > L2"},
+        "ms_isometry_stage_per_move": ms_iso, "ms_svd_calls_summed_per_move": ms_svd,
+        "ms_absorb_per_move": t_step - ms_iso,
+        "contraction_only": {"moves_per_s": world * 1e3 / t_c, "ms_per_move": t_c,
+                             "flops_per_move": gem_fl, "tflops": gem_fl / (t_c * 1e-3) / 1e12,
+                             "frac_of_fp64_peak": gem_fl / (t_c * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                             "note": "isometries injected (INJECT_ISO): chains + corners + commit only, "
+                                     "no reduced env, no SVD"},
+
+        "flops_per_move": F_move,
+        "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
+        "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4)", "achieved": achieved,
+                     "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                     "traffic": None, "launches_per_step": gem_n, "ms_per_step": gem_ms,
+                     "peak_source": "measured DMMA loop (profiles/r01_probe_fp64.txt); MEASURED_PEAKS.json has no FP64"},
+        "e2e": {"value": world * 1e3 / t_e2e, "unit": "moves/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline:
+        s = run_oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": 1.0 / s, "unit": "moves/s", "cores": host_cores(), "kind": "oracle",
+                                "sample": f"1 full left move of {cfg.name} (NumPy/OpenBLAS fp64 oracle, {s:.1f} s)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    cfg = ci.CONFIGS[args.config]
+    if args.impl == "reference":
+        bench_reference(args, cfg)
+    else:
+        bench_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

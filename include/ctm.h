@@ -69,6 +69,8 @@ extern "C" {
 
 /* flags (ctm_params.flags) */
 #define CTM_FLAG_CHECK_FINITE 1   /* scan every committed tensor for NaN/Inf         */
+#define CTM_FLAG_MOVE_ONLY 2      /* size the workspace for moves only (no closures)  */
+#define CTM_FLAG_PROFILE 4        /* time every contraction launch with CUDA events   */
 
 /* reduced-env modes (ctm_reduced_env) */
 #define CTM_RENV_APPROX 0    /* {C'^1, T'^2, C'^2} with side isometries */
@@ -112,12 +114,20 @@ typedef struct {
 /* Per-call statistics (host struct, filled by ctm_left_move / ctm_move). */
 typedef struct {
   double ms_total;      /* device time of the call (CUDA events)                       */
-  double ms_svd;        /* device time inside the SVD stages (cuSOLVER + sign fix)      */
-  double ms_contract;   /* ms_total - ms_svd                                           */
+  double ms_svd;        /* summed device time of the SVD calls (cuSOLVER + sign fix); the
+                           calls of one absorption overlap on worker streams, so this can
+                           exceed ms_isometry                                           */
+  double ms_contract;   /* ms_total - ms_isometry: absorb chains, corners, commit      */
   double flops;         /* algorithmic contraction flops (SURVEY 8(a) closed form)      */
   double min_gap;       /* min sigma_n / sigma_{n+1} over every truncation of the call  */
   int n_svd;            /* SVDs run                                                    */
   int n_kernels;        /* libctm kernels launched (excluding cuSOLVER internals)       */
+  /* CTM_FLAG_PROFILE only: the contraction kernel (tc_gemm) timed launch by launch */
+  double ms_gemm;       /* summed device time of the tc_gemm launches                  */
+  double gemm_flops;    /* their algorithmic flops (sum of 2 M N K)                     */
+  int gemm_launches;    /* number of tc_gemm launches                                  */
+  double ms_isometry;   /* wall device time of the isometry stages (reduced envs + TS,  */
+                        /* rows a1-a5) on the caller's stream, fork to join            */
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by

@@ -9,8 +9,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <limits>
 #include <memory>
+#include <thread>
+#include <exception>
 
 #include "ctm_internal.h"
 
@@ -29,6 +32,16 @@ struct Ten {
     return n;
   }
 };
+
+// ---------------------------------------------------------------------------------------
+// Environment access
+// ---------------------------------------------------------------------------------------
+Ten envC(const ctm_env* e, int x, int k) {
+  return Ten{e->C[x][k - 1], {e->ext[x][k - 1][0], e->ext[x][k - 1][1]}};
+}
+Ten envT(const ctm_env* e, int x, int k, int D) {
+  return Ten{e->T[x][k - 1], {e->ext[x][4 + k - 1][0], D, D, e->ext[x][4 + k - 1][1]}};
+}
 
 Operand op(const std::vector<const Ten*>& ts, const char* lab) {
   Operand o;
@@ -90,7 +103,7 @@ struct ChainJob {
   double* ss;            // nullable: fused sum of squares of res
 };
 
-void chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
+int chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
   const int B = (int)jobs.size();
   const ChainJob& j0 = jobs[0];
   const int D = j0.T->ext[1];
@@ -145,9 +158,10 @@ void chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
   contract(h, op(P([&](int b) { return (const Ten*)&X4[b]; }), "sgjzbc"),
            op(P([&](int b) { return &jobs[b].X->bra; }), "sgjyw"), out(Q(X5), "byzwc"));
   // S6: T'(c,z,w,d) = sum_{b,y} X5(b,y,z,w,c) v2_out(b,y,d)                  K = chi' D
-  contract(h, op(P([&](int b) { return (const Ten*)&X5[b]; }), "byzwc"),
-           op(P([&](int b) { return &jobs[b].outv->v2; }), "byd"), out(res, "czwd", ss));
+  int np = contract(h, op(P([&](int b) { return (const Ten*)&X5[b]; }), "byzwc"),
+                    op(P([&](int b) { return &jobs[b].outv->v2; }), "byd"), out(res, "czwd", ss));
   h.ws.reset(mark);
+  return np;
 }
 
 bool same_shapes(const ChainJob& a, const ChainJob& b) {
@@ -155,12 +169,15 @@ bool same_shapes(const ChainJob& a, const ChainJob& b) {
          a.outv->v1.ext == b.outv->v1.ext && a.outv->v2.ext == b.outv->v2.ext;
 }
 
-void chains(Handle& h, const std::vector<ChainJob>& jobs) {
+// Returns the sum-of-squares partial count of each job's result.
+std::vector<int> chains(Handle& h, const std::vector<ChainJob>& jobs) {
   if (jobs.size() == 2 && same_shapes(jobs[0], jobs[1])) {
-    chain_batch(h, jobs);
-  } else {
-    for (auto& j : jobs) chain_batch(h, {j});
+    int np = chain_batch(h, jobs);
+    return {np, np};
   }
+  std::vector<int> r;
+  for (auto& j : jobs) r.push_back(chain_batch(h, {j}));
+  return r;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -196,26 +213,40 @@ struct RenvOut {
   Iso vl, vr;
 };
 
-RenvOut reduced_env(Handle& h, const RenvIn& in, int chi_pp) {
-  RenvOut o;
+// a1 + a2 for one side: Q = C^1 T^1 (left) or C^2 T^3 (right), then TS(Q; chi'', chi'').
+struct SideOut {
+  Iso v;
+  Ten Q2;   // v^1 contracted into Q: (n1, D, F), reused for C' / C'' (row a4)
+};
+SideOut side_ts(Handle& h, const RenvIn& in, bool left, int chi_pp) {
   const int D = in.T1.ext[1];
-  // a1: Q_l(p,k,b,q) = sum_x C1(x,p) T1(q,k,b,x);  Q_r(p,k,b,q) = sum_x C2(p,x) T3(x,k,b,q)
-  Ten Ql = alloc(h, {in.C1.ext[1], D, D, in.T1.ext[0]});
-  Ten Qr = alloc(h, {in.C2.ext[0], D, D, in.T3.ext[3]});
-  contract(h, op({&in.C1}, "xp"), op({&in.T1}, "qkbx"), out({&Ql}, "pkbq"));
-  contract(h, op({&in.C2}, "px"), op({&in.T3}, "xkbq"), out({&Qr}, "pkbq"));
-  // a2: side isometries (v_l^1, v_l^2), (v_r^1, v_r^2) = TS(Q; chi'', chi'')
-  Ten Q2l, Q2r;
-  o.vl = ts_isometry(h, Ql, chi_pp, chi_pp, &Q2l);
-  o.vr = ts_isometry(h, Qr, chi_pp, chi_pp, &Q2r);
+  SideOut o;
+  if (left) {   // Q_l(p,k,b,q) = sum_x C1(x,p) T1(q,k,b,x)
+    Ten Q = alloc(h, {in.C1.ext[1], D, D, in.T1.ext[0]});
+    contract(h, op({&in.C1}, "xp"), op({&in.T1}, "qkbx"), out({&Q}, "pkbq"));
+    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2);
+  } else {      // Q_r(p,k,b,q) = sum_x C2(p,x) T3(x,k,b,q)
+    Ten Q = alloc(h, {in.C2.ext[0], D, D, in.T3.ext[3]});
+    contract(h, op({&in.C2}, "px"), op({&in.T3}, "xkbq"), out({&Q}, "pkbq"));
+    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2);
+  }
+  return o;
+}
+
+// a3 + a4: M = C' T'^2 C'' from the two side isometries.
+RenvOut renv_finish(Handle& h, const RenvIn& in, const SideOut& L, const SideOut& R) {
+  RenvOut o;
+  o.vl = L.v;
+  o.vr = R.v;
+  const int D = in.T1.ext[1];
   // a3: T'^2 = chain(T^2, X top orientation, in = v_l, out = v_r)
   Ten Tp = alloc(h, {o.vl.v2.ext[2], D, D, o.vr.v2.ext[2]});
   chains(h, {ChainJob{&in.T2, in.X, &o.vl, &o.vr, &Tp, nullptr}});
   // a4: C'(q,l) = sum_{a,b} Q2l(a,b,q) vl2(a,b,l); C''(r,q') = sum vr2(a,b,r) Q2r(a,b,q')
-  Ten Cl = alloc(h, {Q2l.ext[2], o.vl.v2.ext[2]});
-  Ten Cr = alloc(h, {o.vr.v2.ext[2], Q2r.ext[2]});
-  contract(h, op({&Q2l}, "abq"), op({&o.vl.v2}, "abl"), out({&Cl}, "ql"));
-  contract(h, op({&o.vr.v2}, "abr"), op({&Q2r}, "abq"), out({&Cr}, "rq"));
+  Ten Cl = alloc(h, {L.Q2.ext[2], o.vl.v2.ext[2]});
+  Ten Cr = alloc(h, {o.vr.v2.ext[2], R.Q2.ext[2]});
+  contract(h, op({&L.Q2}, "abq"), op({&o.vl.v2}, "abl"), out({&Cl}, "ql"));
+  contract(h, op({&o.vr.v2}, "abr"), op({&R.Q2}, "abq"), out({&Cr}, "rq"));
   //     M(q,k,b,q') = sum_{l,r} C'(q,l) T'(l,k,b,r) C''(r,q')
   Ten M1 = alloc(h, {Cl.ext[0], D, D, Tp.ext[3]});
   contract(h, op({&Cl}, "ql"), op({&Tp}, "lkbr"), out({&M1}, "qkbr"));
@@ -224,38 +255,158 @@ RenvOut reduced_env(Handle& h, const RenvIn& in, int chi_pp) {
   return o;
 }
 
-// ---------------------------------------------------------------------------------------
-// Row a9: corner growth (P:L43, Fig 4(b)).
-// ---------------------------------------------------------------------------------------
-void corner_top_left(Handle& h, const Ten& C1, const Ten& T2, const Iso& v, Ten& res, double* ss) {
-  const int D = T2.ext[1];
-  const size_t mark = h.ws.top;
-  Ten Y1 = alloc(h, {C1.ext[1], D, v.v1.ext[2]});
-  Ten Y2 = alloc(h, {v.v1.ext[2], D, T2.ext[3]});
-  contract(h, op({&C1}, "xp"), op({&v.v1}, "xka"), out({&Y1}, "pka"));
-  contract(h, op({&Y1}, "pka"), op({&T2}, "pkbr"), out({&Y2}, "abr"));
-  contract(h, op({&Y2}, "abr"), op({&v.v2}, "abo"), out({&res}, "or", {ss}));
-  h.ws.reset(mark);
+RenvOut reduced_env(Handle& h, const RenvIn& in, int chi_pp) {
+  SideOut L = side_ts(h, in, true, chi_pp);
+  SideOut R = side_ts(h, in, false, chi_pp);
+  return renv_finish(h, in, L, R);
 }
-void corner_bottom_left(Handle& h, const Ten& C4, const Ten& T4, const Iso& v, Ten& res, double* ss) {
-  const int D = T4.ext[1];
-  const size_t mark = h.ws.top;
-  Ten Y1 = alloc(h, {C4.ext[0], D, v.v1.ext[2]});
-  Ten Y2 = alloc(h, {v.v1.ext[2], D, T4.ext[0]});
-  contract(h, op({&C4}, "px"), op({&v.v1}, "xka"), out({&Y1}, "pka"));
-  contract(h, op({&Y1}, "pka"), op({&T4}, "rkbp"), out({&Y2}, "abr"));
-  contract(h, op({&Y2}, "abr"), op({&v.v2}, "abo"), out({&res}, "ro", {ss}));
-  h.ws.reset(mark);
+
+// Run tasks concurrently, one host thread each (sequentially in the sizing pass).
+void run_parallel(Handle& h, std::vector<std::function<void()>>& tasks) {
+  if (h.dry || tasks.size() == 1) {
+    for (auto& t : tasks) t();
+    return;
+  }
+  std::vector<std::exception_ptr> errs(tasks.size());
+  std::vector<std::thread> th;
+  for (size_t i = 0; i < tasks.size(); ++i)
+    th.emplace_back([&, i]() {
+      try {
+        tasks[i]();
+      } catch (...) {
+        errs[i] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+void sub_begin(Handle& s) {
+  s.ms_svd = 0.0;
+  s.flops = 0.0;
+  s.min_gap = std::numeric_limits<double>::infinity();
+  s.n_svd = 0;
+  s.n_kernels = 0;
+  s.dry = false;
+}
+void sub_merge(Handle& h, Handle& s) {
+  h.ms_svd += s.ms_svd;
+  h.flops += s.flops;
+  h.min_gap = std::min(h.min_gap, s.min_gap);
+  h.n_svd += s.n_svd;
+  h.n_kernels += s.n_kernels;
+  h.kernel_count += s.n_kernels;
+}
+
+// Isometry stage of one column absorption (rows a1-a5) on the worker sub-handles:
+// phase A: the four side TS (x in {a,b}) x (left, right) concurrently;
+// phase B: for each cut type the reduced env M_xy and the main TS(M; chi', chi).
+void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]) {
+  const ctm_params& p = h.prm;
+  const int D = p.D;
+  for (auto& s : h.subs) {
+    sub_begin(*s);
+    s->dry = h.dry;
+    s->ws.reset(0);
+  }
+  if (!h.dry) {
+    CTM_CUDA(cudaEventRecord(h.ev[4], h.stream));   // fork point
+    for (auto& s : h.subs) CTM_CUDA(cudaStreamWaitEvent(s->stream, h.ev[4], 0));
+  }
+  RenvIn ri[2];
+  for (int x = 0; x < 2; ++x)
+    ri[x] = RenvIn{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
+  SideOut side[4];
+  std::vector<std::function<void()>> A;
+  for (int i = 0; i < 4; ++i)
+    A.push_back([&, i]() { side[i] = side_ts(*h.subs[i], ri[i / 2], (i % 2) == 0, p.chi_pp); });
+  run_parallel(h, A);
+  if (!h.dry)
+    for (int x = 0; x < 2; ++x) {   // phase B of x runs on sub 2x and needs sub 2x+1's outputs
+      Handle& r = *h.subs[2 * x + 1];
+      CTM_CUDA(cudaEventRecord(r.ev[0], r.stream));
+      CTM_CUDA(cudaStreamWaitEvent(h.subs[2 * x]->stream, r.ev[0], 0));
+    }
+  std::vector<std::function<void()>> B;
+  for (int x = 0; x < 2; ++x)
+    B.push_back([&, x]() {
+      Handle& s = *h.subs[2 * x];
+      RenvOut ro = renv_finish(s, ri[x], side[2 * x], side[2 * x + 1]);
+      V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr);   // a5
+    });
+  run_parallel(h, B);
+  for (auto& s : h.subs) {
+    if (!h.dry) {
+      CTM_CUDA(cudaEventRecord(s->ev[1], s->stream));   // join
+      CTM_CUDA(cudaStreamWaitEvent(h.stream, s->ev[1], 0));
+    }
+    sub_merge(h, *s);
+  }
+  if (!h.dry) {
+    CTM_CUDA(cudaEventRecord(h.ev[5], h.stream));
+    CTM_CUDA(cudaEventSynchronize(h.ev[5]));
+    float ms = 0.f;
+    CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[4], h.ev[5]));
+    h.ms_iso += ms;
+  }
 }
 
 // ---------------------------------------------------------------------------------------
-// Environment access
+// Row a9: corner growth (P:L43, Fig 4(b)).
 // ---------------------------------------------------------------------------------------
-Ten envC(const ctm_env* e, int x, int k) {
-  return Ten{e->C[x][k - 1], {e->ext[x][k - 1][0], e->ext[x][k - 1][1]}};
+// Batched over jobs with identical shapes (the two windows of an absorption).
+struct CornerJob {
+  Ten C, T;            // top-left: C^1 (d,r), T^2 (l,k,b,r); bottom-left: C^4 (r,u), T^4 (r,k,b,l)
+  const Iso* v;        // projector of the cut the corner row sits on
+  Ten* res;
+  double* ss;
+};
+
+int corner_batch(Handle& h, const std::vector<CornerJob>& jobs, bool top) {
+  const int B = (int)jobs.size();
+  const CornerJob& j0 = jobs[0];
+  const int D = j0.T.ext[1];
+  const size_t mark = h.ws.top;
+  std::vector<Ten> Y1(B), Y2(B);
+  for (int b = 0; b < B; ++b) {
+    Y1[b] = alloc(h, {top ? j0.C.ext[1] : j0.C.ext[0], D, j0.v->v1.ext[2]});
+    Y2[b] = alloc(h, {j0.v->v1.ext[2], D, top ? j0.T.ext[3] : j0.T.ext[0]});
+  }
+  std::vector<const Ten*> c, t, v1, v2, y1c, y2c;
+  std::vector<Ten*> y1, y2, res;
+  std::vector<double*> ss;
+  for (int b = 0; b < B; ++b) {
+    c.push_back(&jobs[b].C);
+    t.push_back(&jobs[b].T);
+    v1.push_back(&jobs[b].v->v1);
+    v2.push_back(&jobs[b].v->v2);
+    y1.push_back(&Y1[b]);
+    y2.push_back(&Y2[b]);
+    y1c.push_back(&Y1[b]);
+    y2c.push_back(&Y2[b]);
+    res.push_back(jobs[b].res);
+    ss.push_back(jobs[b].ss);
+  }
+  // Y1(p,k,a) = sum_x C(x,p) v1(x,k,a)  [top: C^1 (d=x, r=p); bottom: C^4 (r=p, u=x)]
+  contract(h, op(c, top ? "xp" : "px"), op(v1, "xka"), out(y1, "pka"));
+  // Y2(a,b,r) = sum_{p,k} Y1(p,k,a) T(p,k,b,r)  [top: T^2 (l=p,k,b,r); bottom: T^4 (r,k,b,l=p)]
+  contract(h, op(y1c, "pka"), op(t, top ? "pkbr" : "rkbp"), out(y2, "abr"));
+  // C'(o,r) / C'(r,o) = sum_{a,b} Y2(a,b,r) v2(a,b,o)
+  int np = contract(h, op(y2c, "abr"), op(v2, "abo"), out(res, top ? "or" : "ro", ss));
+  h.ws.reset(mark);
+  return np;
 }
-Ten envT(const ctm_env* e, int x, int k, int D) {
-  return Ten{e->T[x][k - 1], {e->ext[x][4 + k - 1][0], D, D, e->ext[x][4 + k - 1][1]}};
+
+std::vector<int> corners(Handle& h, const std::vector<CornerJob>& jobs, bool top) {
+  if (jobs.size() == 2 && jobs[0].C.ext == jobs[1].C.ext && jobs[0].T.ext == jobs[1].T.ext &&
+      jobs[0].v->v1.ext == jobs[1].v->v1.ext && jobs[0].v->v2.ext == jobs[1].v->v2.ext) {
+    int np = corner_batch(h, jobs, top);
+    return {np, np};
+  }
+  std::vector<int> r;
+  for (auto& j : jobs) r.push_back(corner_batch(h, {j}, top));
+  return r;
 }
 
 void check_env(const ctm_env* e, const ctm_params& p) {
@@ -287,15 +438,7 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
       v.v2 = Ten{const_cast<double*>(base + n1), {p.chi_p, D, p.chi}};
     }
   } else {
-    RenvOut ro[2];
-    for (int x = 0; x < 2; ++x) {
-      RenvIn ri{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
-      ro[x] = reduced_env(h, ri, p.chi_pp);
-    }
-    for (int x = 0; x < 2; ++x) {   // a5: main projectors, TS(M; chi', chi)
-      Iso v = ts_isometry(h, ro[x].M, p.chi_p, p.chi, nullptr);
-      V[x][1 - x] = v;
-    }
+    isometry_stage(h, env, st, V);
   }
   if (iso_out) {
     const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
@@ -310,8 +453,7 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
     }
   }
   // new tensors (snapshot semantics: written to workspace, committed at the end)
-  double* ss = h.ws.take(8);
-  zero(h, ss, 6);
+  double* ss = h.ws.take(6 * (size_t)CTM_SS_SLOTS);   // per-tile sum-of-squares partials
   Ten nT[2], nC1[2], nC4[2];
   std::vector<ChainJob> jobs;
   for (int x = 0; x < 2; ++x) {
@@ -325,14 +467,18 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
   Ten T1[2] = {envT(env, 0, 1, D), envT(env, 1, 1, D)};
   for (int x = 0; x < 2; ++x) {
     const int y = 1 - x;
-    jobs.push_back(ChainJob{&T1[x], &sl[x], &V[x][y], &V[y][x], &nT[y], ss + y});
+    jobs.push_back(ChainJob{&T1[x], &sl[x], &V[x][y], &V[y][x], &nT[y], ss + (size_t)y * CTM_SS_SLOTS});
   }
-  chains(h, jobs);
+  std::vector<int> np_t = chains(h, jobs);   // jobs[x] produces nT[y]
+  std::vector<CornerJob> tl, bl;
   for (int x = 0; x < 2; ++x) {
     const int y = 1 - x;
-    corner_top_left(h, envC(env, x, 1), envT(env, x, 2, D), V[y][x], nC1[y], ss + 2 + y);
-    corner_bottom_left(h, envC(env, y, 4), envT(env, y, 4, D), V[y][x], nC4[x], ss + 4 + x);
+    tl.push_back(CornerJob{envC(env, x, 1), envT(env, x, 2, D), &V[y][x], &nC1[y], ss + (size_t)(2 + y) * CTM_SS_SLOTS});
+    bl.push_back(CornerJob{envC(env, y, 4), envT(env, y, 4, D), &V[y][x], &nC4[x], ss + (size_t)(4 + x) * CTM_SS_SLOTS});
   }
+  std::vector<int> np_tl = corners(h, tl, true);   // tl[x] -> nC1[y]
+  std::vector<int> np_bl = corners(h, bl, false);  // bl[x] -> nC4[x]
+  std::vector<int> nparts = {np_t[1], np_t[0], np_tl[1], np_tl[0], np_bl[0], np_bl[1]};
   // K7: normalise + commit (reading R13)
   if (!h.dry) {
     std::vector<const double*> src;
@@ -353,7 +499,7 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
       dst.push_back(env->C[x][3]);
       n.push_back(nC4[x].size());
     }
-    scale_commit(h, src, dst, n, ss);
+    scale_commit(h, src, dst, n, ss, nparts);
     if (p.flags & CTM_FLAG_CHECK_FINITE) {
       int* cnt = reinterpret_cast<int*>(h.dev_scalars);
       CTM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), h.stream));
@@ -558,10 +704,12 @@ int guarded(ctm_handle hh, F&& f) {
 
 void begin_call(Handle& h) {
   h.ms_svd = 0.0;
+  h.ms_iso = 0.0;
   h.flops = 0.0;
   h.min_gap = std::numeric_limits<double>::infinity();
   h.n_svd = 0;
   h.n_kernels = 0;
+  h.prof_used = 0;
   if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
   h.ws.reset(0);
 }
@@ -570,21 +718,42 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   if (!st) return;
   st->ms_total = ms_total;
   st->ms_svd = h.ms_svd;
-  st->ms_contract = ms_total - h.ms_svd;
+  st->ms_isometry = h.ms_iso;
+  st->ms_contract = ms_total - h.ms_iso;
   st->flops = h.flops;
   st->min_gap = h.min_gap;
   st->n_svd = h.n_svd;
   st->n_kernels = h.n_kernels;
+  st->ms_gemm = 0.0;
+  st->gemm_flops = 0.0;
+  st->gemm_launches = h.prof_used;
+  if (h.prof_used) {
+    CTM_CUDA(cudaEventSynchronize(h.prof_ev[2 * h.prof_used - 1]));
+    for (int i = 0; i < h.prof_used; ++i) {
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.prof_ev[2 * i], h.prof_ev[2 * i + 1]));
+      st->ms_gemm += ms;
+      st->gemm_flops += h.prof_flops[i];
+    }
+  }
 }
 
 // Dry run of a representative call sequence to size the workspace.
-size_t size_workspace(Handle& h) {
-  h.dry = true;
-  h.ws.dry = true;
-  h.ws.base = nullptr;
-  h.ws.cap = 0;
+void set_dry(Handle& h, bool on) {
+  h.dry = on;
+  h.ws.dry = on;
   h.ws.reset(0);
   h.ws.peak = 0;
+  if (on) {
+    h.ws.base = nullptr;
+    h.ws.cap = 0;
+  }
+  for (auto& s : h.subs) set_dry(*s, on);
+}
+
+// Dry run of representative call sequences to size the main and the worker arenas.
+void size_workspace(Handle& h) {
+  set_dry(h, true);
   const ctm_params& p = h.prm;
   ctm_env env{};
   static double dummy[1];
@@ -596,17 +765,62 @@ size_t size_workspace(Handle& h) {
     for (int j = 0; j < 8; ++j) env.ext[x][j][0] = env.ext[x][j][1] = p.chi;
   }
   ctm::move_dir(h, CTM_RIGHT, dummy, dummy, &env);
-  size_t need = h.ws.peak;
-  if (!(p.flags & 2)) {
+  size_t main_need = h.ws.peak;
+  size_t sub_need = 0;
+  for (auto& s : h.subs) sub_need = std::max(sub_need, s->ws.peak);
+  // ctm_reduced_env runs the whole reduced env on the main handle
+  h.ws.reset(0);
+  h.ws.peak = 0;
+  {
+    ctm::Site st = ctm::make_site(h, dummy, dummy, p.d, p.D, 2, 1, 4, 3);
+    const int c = p.chi, D = p.D;
+    ctm::RenvIn ri{{dummy, {c, c}}, {dummy, {c, D, D, c}}, {dummy, {c, c}}, {dummy, {c, D, D, c}},
+                   {dummy, {c, D, D, c}}, &st};
+    ctm::reduced_env(h, ri, p.chi_pp);
+  }
+  main_need = std::max(main_need, h.ws.peak);
+  if (!(p.flags & CTM_FLAG_MOVE_ONLY)) {
     h.ws.reset(0);
     h.ws.peak = 0;
     ctm::norm_2x2_impl(h, dummy, dummy, &env, true);
-    need = std::max(need, h.ws.peak);
+    main_need = std::max(main_need, h.ws.peak);
   }
-  h.dry = false;
-  h.ws.dry = false;
-  h.ws.peak = 0;
-  return need + (size_t)64 * 1024 * 1024;   // margin for cuSOLVER size variations
+  set_dry(h, false);
+  const size_t margin = (size_t)32 * 1024 * 1024;   // cuSOLVER workspace size variations
+  h.main_bytes = (main_need + margin + 4095) & ~size_t(4095);
+  h.sub_bytes = (sub_need + margin + 4095) & ~size_t(4095);
+}
+
+void init_solver(Handle& h, const ctm_params* p) {
+  if (cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS) throw Error(CTM_E_SOLVER, "cusolverDnCreate failed");
+  if (cusolverDnCreateParams(&h.solver_params) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(CTM_E_SOLVER, "cusolverDnCreateParams failed");
+  if (cusolverDnCreateGesvdjInfo(&h.gesvdj_info) != CUSOLVER_STATUS_SUCCESS)
+    throw Error(CTM_E_SOLVER, "cusolverDnCreateGesvdjInfo failed");
+  double tol = p->svd_tol > 0 ? p->svd_tol : 2.220446049250313e-16;
+  cusolverDnXgesvdjSetTolerance(h.gesvdj_info, tol);
+  cusolverDnXgesvdjSetMaxSweeps(h.gesvdj_info, 100);
+  cusolverDnSetStream(h.solver, h.stream);
+  CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
+  h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
+  for (auto& e : h.ev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+}
+
+void destroy_handle(Handle& h) {
+  for (auto& s : h.subs) destroy_handle(*s);
+  h.subs.clear();
+  if (h.gesvdj_info) cusolverDnDestroyGesvdjInfo(h.gesvdj_info);
+  if (h.solver_params) cusolverDnDestroyParams(h.solver_params);
+  if (h.solver) cusolverDnDestroy(h.solver);
+  for (auto& e : h.ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h.prof_ev) cudaEventDestroy(e);
+  if (h.dev_scalars) cudaFree(h.dev_scalars);
+  if (h.owns_stream && h.stream) cudaStreamDestroy(h.stream);
+  h.gesvdj_info = nullptr;
+  h.solver_params = nullptr;
+  h.solver = nullptr;
+  h.dev_scalars = nullptr;
 }
 
 }  // namespace
@@ -630,22 +844,21 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
   }
   h.stream = reinterpret_cast<cudaStream_t>(stream);
   try {
-    if (cusolverDnCreate(&h.solver) != CUSOLVER_STATUS_SUCCESS) throw Error(CTM_E_SOLVER, "cusolverDnCreate failed");
-    if (cusolverDnCreateParams(&h.solver_params) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(CTM_E_SOLVER, "cusolverDnCreateParams failed");
-    if (cusolverDnCreateGesvdjInfo(&h.gesvdj_info) != CUSOLVER_STATUS_SUCCESS)
-      throw Error(CTM_E_SOLVER, "cusolverDnCreateGesvdjInfo failed");
-    double tol = p->svd_tol > 0 ? p->svd_tol : 2.220446049250313e-16;
-    cusolverDnXgesvdjSetTolerance(h.gesvdj_info, tol);
-    cusolverDnXgesvdjSetMaxSweeps(h.gesvdj_info, 100);
-    cusolverDnSetStream(h.solver, h.stream);
-    CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
-    h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
-    for (auto& e : h.ev) CTM_CUDA(cudaEventCreate(&e));
-    size_t need = size_workspace(h);
-    if (ws_bytes) *ws_bytes = need;
+    init_solver(h, &h.prm);
+    for (int i = 0; i < 4; ++i) {   // workers of the isometry stage (4 side TS, 2 main TS)
+      std::unique_ptr<Handle> s(new Handle());
+      s->prm = h.prm;
+      s->prm.flags &= ~CTM_FLAG_PROFILE;
+      CTM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+      s->owns_stream = true;
+      init_solver(*s, &s->prm);
+      h.subs.push_back(std::move(s));
+    }
+    size_workspace(h);
+    if (ws_bytes) *ws_bytes = h.main_bytes + h.subs.size() * h.sub_bytes;
   } catch (const Error& e) {
     fprintf(stderr, "ctm_init: %s\n", e.what());
+    destroy_handle(h);
     return e.code;
   }
   *out = hh.release();
@@ -655,9 +868,18 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
 int ctm_set_workspace(ctm_handle hh, void* dev, size_t bytes) {
   return guarded(hh, [&](Handle& h) {
     if (!dev) throw Error(CTM_E_ARG, "null workspace");
-    h.ws.base = static_cast<char*>(dev);
-    h.ws.cap = bytes;
+    const size_t need = h.main_bytes + h.subs.size() * h.sub_bytes;
+    if (bytes < need) throw Error(CTM_E_NOMEM, "workspace smaller than ctm_init reported");
+    char* base = static_cast<char*>(dev);
+    h.ws.base = base;
+    h.ws.cap = h.main_bytes;
     h.ws.reset(0);
+    for (size_t i = 0; i < h.subs.size(); ++i) {
+      Handle& s = *h.subs[i];
+      s.ws.base = base + h.main_bytes + i * h.sub_bytes;
+      s.ws.cap = h.sub_bytes;
+      s.ws.reset(0);
+    }
   });
 }
 
@@ -670,13 +892,8 @@ int ctm_set_stream(ctm_handle hh, uintptr_t stream) {
 
 int ctm_destroy(ctm_handle hh) {
   if (!hh) return CTM_E_ARG;
-  Handle& h = hh->h;
-  if (h.gesvdj_info) cusolverDnDestroyGesvdjInfo(h.gesvdj_info);
-  if (h.solver_params) cusolverDnDestroyParams(h.solver_params);
-  if (h.solver) cusolverDnDestroy(h.solver);
-  for (auto& e : h.ev)
-    if (e) cudaEventDestroy(e);
-  if (h.dev_scalars) cudaFree(h.dev_scalars);
+  cudaStreamSynchronize(hh->h.stream);
+  destroy_handle(hh->h);
   delete hh;
   return CTM_OK;
 }

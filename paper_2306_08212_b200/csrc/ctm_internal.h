@@ -4,6 +4,7 @@
 #include <cusolverDn.h>
 
 #include <cstdint>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -49,7 +50,8 @@ struct Arena {
     if (!dry && top + bytes > cap)
       throw Error(CTM_E_NOMEM, "workspace too small: need > " + std::to_string(top + bytes) +
                                    " bytes, have " + std::to_string(cap));
-    double* r = dry ? nullptr : reinterpret_cast<double*>(base + top);
+    // sizing pass: a fake, never dereferenced, non-null address
+    double* r = reinterpret_cast<double*>((dry ? reinterpret_cast<char*>(4096) : base) + top);
     top += bytes;
     if (top > peak) peak = top;
     return r;
@@ -67,22 +69,35 @@ struct Handle {
   std::vector<char> host_buf;          // cuSOLVER host workspace
   int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
   double* dev_scalars = nullptr;        // small device scratch (norms etc.)
-  cudaEvent_t ev[4]{};
+  cudaEvent_t ev[6]{};
   std::string last_error;
   int64_t kernel_count = 0;
   // per-call statistics
   double ms_svd = 0.0;
+  double ms_iso = 0.0;                  // isometry-stage wall time (fork -> join)
   double flops = 0.0;
   double min_gap = 1e300;
   int n_svd = 0;
   int n_kernels = 0;
   bool dry = false;                     // sizing pass: no launches
+  // CTM_FLAG_PROFILE: event pairs around each tc_gemm launch
+  std::vector<cudaEvent_t> prof_ev;
+  std::vector<double> prof_flops;
+  int prof_used = 0;
+  // worker sub-handles (own stream + cuSOLVER handle + workspace slice) for the
+  // independent isometry tasks of a column absorption; cuSOLVER blocks the calling host
+  // thread, so each worker is driven by its own host thread.
+  std::vector<std::unique_ptr<Handle>> subs;
+  size_t main_bytes = 0, sub_bytes = 0;
+  bool owns_stream = false;
   void count_kernel(int n = 1) { kernel_count += n; n_kernels += n; }
 };
 
-// tc_gemm.cu
-void contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
-              double alpha = 1.0);
+// tc_gemm.cu: returns the number of sum-of-squares partials written per problem (slots
+// 0..n-1 of C.sumsq[b]; at most CTM_SS_SLOTS).
+constexpr int CTM_SS_SLOTS = 4096;
+int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
+             double alpha = 1.0);
 
 // kernels.cu
 void permute(Handle& h, const double* src, const std::vector<int>& ext, const std::vector<int>& perm,
@@ -90,8 +105,9 @@ void permute(Handle& h, const double* src, const std::vector<int>& ext, const st
 void zero(Handle& h, double* p, size_t n);
 void sumsq(Handle& h, const std::vector<const double*>& srcs, const std::vector<size_t>& ns,
            double* out);
+// dst[i] = src[i] / sqrt(sum_{j < nparts[i]} ss[i*CTM_SS_SLOTS + j]) (partials summed in order)
 void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
-                  const std::vector<size_t>& ns, const double* sumsqs);
+                  const std::vector<size_t>& ns, const double* ss, const std::vector<int>& nparts);
 void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count);
 void abs_copy(Handle& h, const double* src, double* dst, size_t n);
 void dot(Handle& h, const double* a, const double* b, size_t n, double* out);   // out = a.b (device)

@@ -34,6 +34,10 @@ __global__ void zero_kernel(double* p, long long n) {
     p[i] = 0.0;
 }
 
+struct Parts {
+  int n[8];
+};
+
 struct Multi {
   const double* src[8];
   double* dst[8];
@@ -62,10 +66,19 @@ __global__ void sumsq_kernel(Multi m, double* out) {
   }
 }
 
-// dst[y][i] = src[y][i] / sqrt(sumsq[y])   (Frobenius normalisation, reading R13)
-__global__ void scale_commit_kernel(Multi m, const double* __restrict__ ss) {
+// dst[y][i] = src[y][i] / ||src[y]||_F   (Frobenius normalisation, reading R13); the norm
+// is the in-order sum of the per-tile partials written by the producing GEMM (deterministic).
+__global__ void scale_commit_kernel(Multi m, const double* __restrict__ ss, Parts parts) {
   const int y = blockIdx.y;
-  const double inv = rsqrt(ss[y]);
+  __shared__ double inv_s;
+  if (threadIdx.x == 0) {
+    const double* p = ss + (size_t)y * CTM_SS_SLOTS;
+    double acc = 0.0;
+    for (int j = 0; j < parts.n[y]; ++j) acc += p[j];
+    inv_s = 1.0 / sqrt(acc);
+  }
+  __syncthreads();
+  const double inv = inv_s;
   const double* __restrict__ s = m.src[y];
   double* __restrict__ d = m.dst[y];
   const long long n = m.n[y];
@@ -159,8 +172,10 @@ void sumsq(Handle& h, const std::vector<const double*>& srcs, const std::vector<
 }
 
 void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::vector<double*>& dsts,
-                  const std::vector<size_t>& ns, const double* ss) {
+                  const std::vector<size_t>& ns, const double* ss, const std::vector<int>& nparts) {
   if (h.dry) return;
+  Parts parts{};
+  for (size_t i = 0; i < nparts.size(); ++i) parts.n[i] = nparts[i];
   Multi m{};
   long long mx = 0;
   for (size_t i = 0; i < srcs.size(); ++i) {
@@ -170,7 +185,7 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
     mx = std::max(mx, m.n[i]);
   }
   dim3 grid(std::min(grid_for(mx), kSMs * 2), (unsigned)srcs.size());
-  scale_commit_kernel<<<grid, 256, 0, h.stream>>>(m, ss);
+  scale_commit_kernel<<<grid, 256, 0, h.stream>>>(m, ss, parts);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }

@@ -9,6 +9,27 @@
 namespace ctm {
 namespace {
 
+// Split-K reduction: C[off(m,n)] = alpha * sum_s P[b][s][m][n] (+ beta C), in split order.
+__global__ void splitk_reduce_kernel(const TcArgs args) {
+  const int b = blockIdx.y;
+  const long long MN = (long long)args.M * args.N;
+  double ss = 0.0;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN; e += (long long)gridDim.x * blockDim.x) {
+    const double* P = args.part + (size_t)b * args.splits * MN + e;
+    double v = 0.0;
+    for (int s = 0; s < args.splits; ++s) v += P[(size_t)s * MN];
+    const int m = (int)(e / args.N), n = (int)(e - (long long)m * args.N);
+    const int off = tc::mode_offset(m, args.nm, args.m_ext, args.c_m) + tc::mode_offset(n, args.nn, args.n_ext, args.c_n);
+    v *= args.alpha;
+    if (args.beta != 0.0) v += args.beta * args.C[b][off];
+    args.C[b][off] = v;
+    ss += v * v;
+  }
+  if (args.sumsq[b] != nullptr) tc::block_sum_store(ss, args.sumsq[b] + blockIdx.x);
+}
+
+
+
 struct Leg {
   char c;
   int ext;
@@ -59,30 +80,52 @@ ModeOut build_modes(std::vector<Leg> legs, int key, int op1, int op2) {
   return mo;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST>
-void launch_cfg(Handle& h, const TcArgs& a, int batch) {
-  using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST>;
-  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST>;
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
+void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
+  using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
+  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>;
   static bool attr_set = false;
   if (!attr_set) {
     CTM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
     attr_set = true;
   }
-  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, batch);
+  dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
   kern<<<grid, C_::THREADS, C_::SMEM_BYTES, h.stream>>>(a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
 
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+void launch_cfg(Handle& h, const TcArgs& a, int gz) {
+  if (a.a_kfast) {
+    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, true>(h, a, gz);
+    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, false>(h, a, gz);
+  } else {
+    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, true>(h, a, gz);
+    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, false>(h, a, gz);
+  }
+}
+
 struct CfgInfo {
   int BM, BN;
+  int per_sm;   // resident CTAs per SM
   double eff;   // relative per-tile efficiency (bigger tiles reuse operands more)
 };
-const CfgInfo kCfgs[] = {{128, 128, 1.00}, {128, 64, 0.92}, {64, 128, 0.92}, {64, 64, 0.80}};
+// 0: 128x64 (8 warps 4x2), 1: 64x128 (8 warps 2x4), 2: 64x64 (4 warps 2x2); warp tile 32x32
+const CfgInfo kCfgs[] = {{128, 64, 2, 1.00}, {64, 128, 2, 1.00}, {64, 64, 3, 0.85}};
+constexpr int kSMs = 148;
+
+void launch_idx(Handle& h, int idx, const TcArgs& a, int gz) {
+  switch (idx) {
+    case 0: launch_cfg<128, 64, 16, 4, 2, 3, 2>(h, a, gz); break;
+    case 1: launch_cfg<64, 128, 16, 2, 4, 3, 2>(h, a, gz); break;
+    default: launch_cfg<64, 64, 16, 2, 2, 3, 3>(h, a, gz); break;
+  }
+}
 
 }  // namespace
 
-void contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C, double alpha) {
+int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C, double alpha) {
   const int batch = (int)C.p.size();
   if (batch < 1 || batch > CTM_MAXBATCH || (int)A.p.size() != batch || (int)B.p.size() != batch)
     throw Error(CTM_E_ARG, "contract: bad batch");
@@ -184,7 +227,7 @@ void contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C
   }
   a.a_kfast = a_kfast;
   a.b_kfast = b_kfast;
-  a.c_nfast = c_nfast;
+  (void)c_nfast;
   a.alpha = alpha;
   a.beta = 0.0;
   for (int b = 0; b < batch; ++b) {
@@ -194,44 +237,101 @@ void contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C
     a.sumsq[b] = C.sumsq.empty() ? nullptr : C.sumsq[b];
   }
   h.flops += 2.0 * (double)M * (double)N * (double)K * batch;
-  if (h.dry) return;
-  // tile-config choice: maximise (wave efficiency) x (tile fill) x (per-tile efficiency)
-  int best = 0;
+  a.splits = 1;
+  a.ktiles_per_split = (int)((K + 15) / 16);
+  a.part = nullptr;
+  if (h.dry) {
+    // sizing pass: reserve the largest split-K slab this contraction could use
+    const size_t mark = h.ws.top;
+    h.ws.take((size_t)batch * 8 * M * N);
+    h.ws.reset(mark);
+    return 0;
+  }
+  // tile-config choice: maximise (wave efficiency) x (tile fill) x (per-tile efficiency),
+  // then split K when one wave is not filled (deterministic split-K reduction).
+  int best = 0, best_splits = 1;
   double best_score = -1;
-  for (int i = 0; i < 4; ++i) {
+  const long long ktiles_all = (K + 15) / 16;
+  for (int i = 0; i < 3; ++i) {
     const CfgInfo& c = kCfgs[i];
     long long tm = (M + c.BM - 1) / c.BM, tn = (N + c.BN - 1) / c.BN;
     long long tiles = tm * tn * batch;
+    const long long slots = (long long)kSMs * c.per_sm;
+    int splits = 1;
+    if (tiles < slots && K <= CTM_KTAB_MAX) {
+      long long want = (2 * slots + tiles - 1) / tiles;
+      splits = (int)std::max(1LL, std::min({want, 8LL, ktiles_all / 4}));
+    }
+    long long ctas = tiles * splits;
     double fill = (double)M * N / ((double)tm * c.BM * tn * c.BN);
-    long long waves = (tiles + 147) / 148;
-    double wave_eff = (double)tiles / (waves * 148.0);
-    double score = fill * wave_eff * c.eff;
+    long long waves = (ctas + slots - 1) / slots;
+    double wave_eff = (double)ctas / (waves * (double)slots);
+    double split_cost = splits > 1 ? 0.97 : 1.0;
+    double score = fill * wave_eff * c.eff * split_cost;
     if (score > best_score + 1e-9) {
       best_score = score;
       best = i;
+      best_splits = splits;
     }
   }
+  const bool prof = (h.prm.flags & CTM_FLAG_PROFILE) != 0;
+  auto prof_begin = [&]() {
+    if (!prof) return;
+    if ((int)h.prof_ev.size() < 2 * (h.prof_used + 1)) {
+      for (int i = 0; i < 256; ++i) {
+        cudaEvent_t e;
+        CTM_CUDA(cudaEventCreate(&e));
+        h.prof_ev.push_back(e);
+      }
+    }
+    CTM_CUDA(cudaEventRecord(h.prof_ev[2 * h.prof_used], h.stream));
+  };
+  auto prof_end = [&](double flops) {
+    if (!prof) return;
+    CTM_CUDA(cudaEventRecord(h.prof_ev[2 * h.prof_used + 1], h.stream));
+    if ((int)h.prof_flops.size() <= h.prof_used) h.prof_flops.resize(h.prof_used + 1);
+    h.prof_flops[h.prof_used] = flops;
+    ++h.prof_used;
+  };
+  if (best_splits > 1) {
+    const size_t mark = h.ws.top;
+    a.splits = best_splits;
+    a.ktiles_per_split = (int)((ktiles_all + best_splits - 1) / best_splits);
+    a.part = h.ws.take((size_t)batch * best_splits * M * N);
+    prof_begin();
+    launch_idx(h, best, a, batch * best_splits);
+    int rb = (int)std::min<long long>(2 * kSMs, ((long long)M * N + 255) / 256);
+    splitk_reduce_kernel<<<dim3(rb, batch), 256, 0, h.stream>>>(a);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+    prof_end(2.0 * (double)M * N * K * batch);
+    h.ws.reset(mark);
+    return rb;
+  }
+  // K beyond the shared-memory offset table: chunk the slowest k mode (beta = 1)
   const long long chunk = K > CTM_KTAB_MAX ? CTM_KTAB_MAX / k_inner : k_last;
   const int lk = a.nk - 1;
   const long long sa_last = mk.s1[lk], sb_last = mk.s2[lk];
+  int nparts = 0;
   for (long long j0 = 0; j0 < k_last; j0 += chunk) {
     TcArgs c = a;
     const long long len = std::min(chunk, k_last - j0);
     c.k_ext[lk] = (int)len;
     c.K = (int)(k_inner * len);
     c.beta = j0 == 0 ? 0.0 : 1.0;
+    c.splits = 1;
+    c.ktiles_per_split = (c.K + 15) / 16;
     for (int b = 0; b < batch; ++b) {
       c.A[b] = a.A[b] + j0 * sa_last;
       c.B[b] = a.B[b] + j0 * sb_last;
       c.sumsq[b] = (j0 + len >= k_last) ? a.sumsq[b] : nullptr;
     }
-    switch (best) {
-      case 0: launch_cfg<128, 128, 16, 2, 4, 3>(h, c, batch); break;
-      case 1: launch_cfg<128, 64, 16, 2, 2, 4>(h, c, batch); break;
-      case 2: launch_cfg<64, 128, 16, 2, 2, 4>(h, c, batch); break;
-      default: launch_cfg<64, 64, 16, 2, 2, 4>(h, c, batch); break;
-    }
+    prof_begin();
+    launch_idx(h, best, c, batch);
+    prof_end(2.0 * (double)c.M * c.N * c.K * batch);
+    nparts = (int)(((M + kCfgs[best].BM - 1) / kCfgs[best].BM) * ((N + kCfgs[best].BN - 1) / kCfgs[best].BN));
   }
+  return nparts;
 }
 
 }  // namespace ctm

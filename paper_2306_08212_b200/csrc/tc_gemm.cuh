@@ -1,6 +1,6 @@
 // tc_gemm.cuh -- FP64 tensor-contraction GEMM on the B200 DMMA pipe (sm_100a).
 //
-//   C[m, n] = alpha * sum_k A[m, k] * B[k, n]
+//   C[m, n] = alpha * sum_k A[m, k] * B[k, n]  (+ beta * C)
 //
 // where m, n and k are multi-indices of up to CTM_MAXMODES modes each and every operand
 // is addressed through per-mode element strides, so the index permutations of the
@@ -10,36 +10,46 @@
 // Design:
 //  * math: mma.sync.aligned.m8n8k4.row.col.f64 -> SASS DMMA.8x8x4.  sm_100a has no
 //    tcgen05 FP64 kind (ptxas rejects .kind::f64) and wgmma is sm_90a-only, so DMMA is
-//    the FP64 tensor path; measured 37.1 TFLOP/s peak (= DFMA peak) on this B200.
-//  * operand staging: cp.async (LDGSTS, 8 B) gathers from per-mode offset tables kept in
-//    shared memory, multi-stage pipeline; the load thread mapping follows whichever index
-//    is contiguous in global memory (m- or k-fast for A, k- or n-fast for B) so every
-//    warp load is coalesced.
-//  * epilogue: accumulators -> shared memory -> global in the order of C's contiguous
-//    mode (coalesced stores for either layout), optional fused sum of squares for the
-//    Frobenius normalisation (reading R13) accumulated per problem with atomics.
-//  * batch: blockIdx.z selects one of up to CTM_MAXBATCH problems sharing shapes and
-//    strides (the two chains / corners of an absorption run in one launch).
+//    the FP64 tensor path; measured 37.1 TFLOP/s peak (= DFMA peak) on this B200, and
+//    reached with as few as 4 warps/SM (profiles/r01_probe_dmma_occupancy.txt).
+//  * two CTAs per SM (warp tile 32x32, <= 128 registers, ~100 KB shared memory each) so
+//    one CTA's prologue / epilogue / load bursts overlap the other's DMMA stream (the
+//    first version, one 128x128 CTA per SM, left the DMMA pipe idle ~47% of the time:
+//    profiles/r01_ncu_c4_chain_v1.txt).
+//  * operand staging: cp.async (LDGSTS, 8 B) gathers, 3-stage pipeline; each thread's
+//    fixed row/column offsets live in registers, the k offsets in a shared-memory table;
+//    the thread mapping follows the operand's contiguous index (m/k-fast for A, k/n-fast
+//    for B) so every warp load is coalesced.
+//  * epilogue: direct stores from the DMMA accumulator layout through per-row/column
+//    offset tables (any output permutation), fused sum of squares for the Frobenius
+//    normalisation (reading R13).
+//  * split-K (grid.z = batch x splits) for the small-M*N, large-K contractions (S3, S6,
+//    corners): partial tiles go to a workspace slab and a deterministic reduction kernel
+//    sums them in split order (no floating-point atomics on the data).
+//  * batch: one launch serves up to CTM_MAXBATCH problems with identical shapes/strides.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
 
 #define CTM_MAXMODES 4
 #define CTM_MAXBATCH 4
-#define CTM_KTAB_MAX 4096
+#define CTM_KTAB_MAX 2048
 
 struct TcArgs {
   const double* A[CTM_MAXBATCH];
   const double* B[CTM_MAXBATCH];
   double* C[CTM_MAXBATCH];
-  double* sumsq[CTM_MAXBATCH];   // nullable: += sum of squares of the written tile
+  double* sumsq[CTM_MAXBATCH];   // nullable: per-CTA partial sums of squares of the final C values,
+                                 // slot blockIdx.y*gridDim.x+blockIdx.x (deterministic reduction later)
+  double* part;                  // split-K partial slab [batch][split][M][N] (splits > 1)
   int M, N, K;
   int nm, nn, nk;
   int m_ext[CTM_MAXMODES], n_ext[CTM_MAXMODES], k_ext[CTM_MAXMODES];
   int a_m[CTM_MAXMODES], a_k[CTM_MAXMODES];
   int b_k[CTM_MAXMODES], b_n[CTM_MAXMODES];
   int c_m[CTM_MAXMODES], c_n[CTM_MAXMODES];
-  int a_kfast, b_kfast, c_nfast;
+  int a_kfast, b_kfast;
+  int splits, ktiles_per_split;
   double alpha;
   double beta;     // C = alpha*A*B + beta*C (beta != 0 only for K-chunked accumulation)
 };
@@ -60,10 +70,8 @@ __device__ __forceinline__ int mode_offset(int idx, int nmodes, const int* ext, 
   return off;
 }
 
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem, bool pred) {
-  unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  int n = pred ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(n));
+__device__ __forceinline__ void cp_async8(unsigned smem_addr, const void* gmem, int bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_addr), "l"(gmem), "r"(bytes));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -75,51 +83,70 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+// Deterministic block sum (warp shuffles, then warps in order) stored by thread 0.
+__device__ __forceinline__ void block_sum_store(double v, double* out) {
+  __shared__ double red[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+    *out = s;
+  }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
 struct Cfg {
   static constexpr int THREADS = 32 * WM * WN;
   static constexpr int WTM = BM / WM;           // warp tile
   static constexpr int WTN = BN / WN;
   static constexpr int MT = WTM / 8;            // 8x8 mma tiles per warp
   static constexpr int NT = WTN / 8;
-  static constexpr int PADA = 8, PADB = 8, PADC = 1;
-  static constexpr int LDA = BM + PADA;         // smem row (k) stride, doubles
-  static constexpr int LDB = BN + PADB;
-  static constexpr int LDC = BN + PADC;
+  static constexpr int PAD = 8;
+  static constexpr int LDA = BM + PAD;          // smem row (k) stride, doubles
+  static constexpr int LDB = BN + PAD;
   static constexpr int STAGE_DOUBLES = BK * LDA + BK * LDB;
   static constexpr int PIPE_BYTES = STAGES * STAGE_DOUBLES * 8;
-  static constexpr int EPI_BYTES = BM * LDC * 8;
-  static constexpr int MAIN_BYTES = PIPE_BYTES > EPI_BYTES ? PIPE_BYTES : EPI_BYTES;
-  // tables: A row offsets (BM), B col offsets (BN), C row/col offsets, K tables
   static constexpr int TAB_BYTES = (2 * BM + 2 * BN) * 4 + 2 * CTM_KTAB_MAX * 4;
-  static constexpr int SMEM_BYTES = MAIN_BYTES + TAB_BYTES;
-  static_assert(THREADS % BM == 0 || BM % (THREADS / BK) == 0, "A mapping");
+  static constexpr int SMEM_BYTES = PIPE_BYTES + TAB_BYTES;
+  static constexpr int A_PER = BM * BK / THREADS;   // A elements per thread per stage
+  static constexpr int B_PER = BN * BK / THREADS;
   static_assert((BM * BK) % THREADS == 0 && (BN * BK) % THREADS == 0, "tile/threads");
+  static_assert(THREADS % BK == 0 && THREADS % BM == 0 && THREADS % BN == 0, "mapping");
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "mma tiling");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(32 * WM * WN, 1) tc_gemm_kernel(const TcArgs args) {
-  using C_ = Cfg<BM, BN, BK, WM, WN, STAGES>;
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool AKF, bool BKF>
+__global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArgs args) {
+  using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   constexpr int THREADS = C_::THREADS;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* pipe = reinterpret_cast<double*>(smem_raw);
-  int* tab = reinterpret_cast<int*>(smem_raw + C_::MAIN_BYTES);
+  int* tab = reinterpret_cast<int*>(smem_raw + C_::PIPE_BYTES);
   int* a_moff = tab;                 // BM
   int* b_noff = a_moff + BM;         // BN
   int* c_moff = b_noff + BN;         // BM
   int* c_noff = c_moff + BM;         // BN
-  int* a_koff = c_noff + BN;         // K (<= CTM_KTAB_MAX)
+  int* a_koff = c_noff + BN;         // K range of this split (<= CTM_KTAB_MAX)
   int* b_koff = a_koff + CTM_KTAB_MAX;
 
   const int tid = threadIdx.x;
-  const int bz = blockIdx.z;
+  const int bz = blockIdx.z / args.splits;
+  const int split = blockIdx.z - bz * args.splits;
   const int m0 = blockIdx.y * BM;
   const int n0 = blockIdx.x * BN;
   const int M = args.M, N = args.N, K = args.K;
+  const int kt_begin = split * args.ktiles_per_split;
+  const int kt_total = (K + BK - 1) / BK;
+  const int kt_end = min(kt_total, kt_begin + args.ktiles_per_split);
+  const int ktiles = max(0, kt_end - kt_begin);
+  const int kbase = kt_begin * BK;
+  const int kcount = min(K - kbase, ktiles * BK);
   const double* __restrict__ Ag = args.A[bz];
   const double* __restrict__ Bg = args.B[bz];
-  double* __restrict__ Cg = args.C[bz];
 
   // ---- offset tables -------------------------------------------------------------
   for (int i = tid; i < BM; i += THREADS) {
@@ -134,69 +161,52 @@ __global__ void __launch_bounds__(32 * WM * WN, 1) tc_gemm_kernel(const TcArgs a
     b_noff[i] = ok ? mode_offset(n, args.nn, args.n_ext, args.b_n) : -1;
     c_noff[i] = ok ? mode_offset(n, args.nn, args.n_ext, args.c_n) : -1;
   }
-  for (int k = tid; k < K; k += THREADS) {
-    a_koff[k] = mode_offset(k, args.nk, args.k_ext, args.a_k);
-    b_koff[k] = mode_offset(k, args.nk, args.k_ext, args.b_k);
+  for (int k = tid; k < kcount; k += THREADS) {
+    a_koff[k] = mode_offset(kbase + k, args.nk, args.k_ext, args.a_k);
+    b_koff[k] = mode_offset(kbase + k, args.nk, args.k_ext, args.b_k);
   }
   __syncthreads();
 
-  const int ktiles = (K + BK - 1) / BK;
+  // ---- per-thread load assignment (fixed across stages) -----------------------------
+  // A: k-fast -> fixed kl, rows ml0 + j*(THREADS/BK);  m-fast -> fixed ml, kl0 + j*(THREADS/BM)
+  constexpr bool akf = AKF, bkf = BKF;
+  const int a_fix = akf ? (tid % BK) : (tid % BM);
+  const int a_var0 = akf ? (tid / BK) : (tid / BM);
+  const int a_step = akf ? (THREADS / BK) : (THREADS / BM);
+  const int b_fix = bkf ? (tid % BK) : (tid % BN);
+  const int b_var0 = bkf ? (tid / BK) : (tid / BN);
+  const int b_step = bkf ? (THREADS / BK) : (THREADS / BN);
+  int a_row[C_::A_PER];   // k-fast: offsets of my rows; m-fast: only a_row[0] used
+  int b_col[C_::B_PER];
+#pragma unroll
+  for (int j = 0; j < C_::A_PER; ++j) a_row[j] = akf ? a_moff[a_var0 + j * a_step] : a_moff[a_fix];
+#pragma unroll
+  for (int j = 0; j < C_::B_PER; ++j) b_col[j] = bkf ? b_noff[b_var0 + j * b_step] : b_noff[b_fix];
+  const unsigned pipe_s = static_cast<unsigned>(__cvta_generic_to_shared(pipe));
 
   auto load_stage = [&](int stage, int kt) {
-    double* As = pipe + stage * C_::STAGE_DOUBLES;
-    double* Bs = As + BK * C_::LDA;
-    const int k0 = kt * BK;
-    // A tile: BM x BK -> As[k][m]
-    if (args.a_kfast) {
-      constexpr int ROWS_PER = THREADS / BK;
+    const unsigned As = pipe_s + stage * C_::STAGE_DOUBLES * 8;
+    const unsigned Bs = As + BK * C_::LDA * 8;
+    const int k0 = kt * BK;   // relative to kbase
 #pragma unroll
-      for (int j = 0; j < (BM * BK) / THREADS; ++j) {
-        int kl = tid % BK;
-        int ml = tid / BK + j * ROWS_PER;
-        int k = k0 + kl;
-        int mo = a_moff[ml];
-        bool ok = (k < K) && (mo >= 0);
-        const double* src = ok ? Ag + (mo + a_koff[k]) : Ag;
-        cp_async8(As + kl * C_::LDA + ml, src, ok);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < (BM * BK) / THREADS; ++j) {
-        int e = tid + j * THREADS;
-        int ml = e % BM;
-        int kl = e / BM;
-        int k = k0 + kl;
-        int mo = a_moff[ml];
-        bool ok = (k < K) && (mo >= 0);
-        const double* src = ok ? Ag + (mo + a_koff[k]) : Ag;
-        cp_async8(As + kl * C_::LDA + ml, src, ok);
-      }
+    for (int j = 0; j < C_::A_PER; ++j) {
+      const int kl = akf ? a_fix : (a_var0 + j * a_step);
+      const int ml = akf ? (a_var0 + j * a_step) : a_fix;
+      const int k = k0 + kl;
+      const int ro = a_row[akf ? j : 0];
+      const bool ok = (k < kcount) & (ro >= 0);
+      const double* src = Ag + (ok ? ro + a_koff[k] : 0);
+      cp_async8(As + (kl * C_::LDA + ml) * 8, src, ok ? 8 : 0);
     }
-    // B tile: BK x BN -> Bs[k][n]
-    if (args.b_kfast) {
-      constexpr int COLS_PER = THREADS / BK;
 #pragma unroll
-      for (int j = 0; j < (BN * BK) / THREADS; ++j) {
-        int kl = tid % BK;
-        int nl = tid / BK + j * COLS_PER;
-        int k = k0 + kl;
-        int no = b_noff[nl];
-        bool ok = (k < K) && (no >= 0);
-        const double* src = ok ? Bg + (no + b_koff[k]) : Bg;
-        cp_async8(Bs + kl * C_::LDB + nl, src, ok);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < (BN * BK) / THREADS; ++j) {
-        int e = tid + j * THREADS;
-        int nl = e % BN;
-        int kl = e / BN;
-        int k = k0 + kl;
-        int no = b_noff[nl];
-        bool ok = (k < K) && (no >= 0);
-        const double* src = ok ? Bg + (no + b_koff[k]) : Bg;
-        cp_async8(Bs + kl * C_::LDB + nl, src, ok);
-      }
+    for (int j = 0; j < C_::B_PER; ++j) {
+      const int kl = bkf ? b_fix : (b_var0 + j * b_step);
+      const int nl = bkf ? (b_var0 + j * b_step) : b_fix;
+      const int k = k0 + kl;
+      const int co = b_col[bkf ? j : 0];
+      const bool ok = (k < kcount) & (co >= 0);
+      const double* src = Bg + (ok ? co + b_koff[k] : 0);
+      cp_async8(Bs + (kl * C_::LDB + nl) * 8, src, ok ? 8 : 0);
     }
   };
 
@@ -241,50 +251,52 @@ __global__ void __launch_bounds__(32 * WM * WN, 1) tc_gemm_kernel(const TcArgs a
     }
   }
   cp_async_wait<0>();
-  __syncthreads();
 
-  // ---- epilogue: registers -> smem -> global (C's contiguous order) ------------------
-  double* Cs = pipe;
+  // ---- epilogue: direct stores from the accumulator layout ---------------------------
   const double alpha = args.alpha, beta = args.beta;
+  double ss = 0.0;
+  if (args.splits > 1) {
+    double* __restrict__ P = args.part + ((size_t)blockIdx.z * M) * N;
 #pragma unroll
-  for (int i = 0; i < C_::MT; ++i)
+    for (int i = 0; i < C_::MT; ++i) {
+      const int m = m0 + wm * C_::WTM + i * 8 + g;
+#pragma unroll
+      for (int j = 0; j < C_::NT; ++j) {
+        const int n = n0 + wn * C_::WTN + j * 8 + 2 * t;
+        if (m < M) {
+          if (n < N) P[(size_t)m * N + n] = acc[i][j][0];
+          if (n + 1 < N) P[(size_t)m * N + n + 1] = acc[i][j][1];
+        }
+      }
+    }
+    return;
+  }
+  double* __restrict__ Cg = args.C[bz];
+#pragma unroll
+  for (int i = 0; i < C_::MT; ++i) {
+    const int r = wm * C_::WTM + i * 8 + g;
+    const int mo = c_moff[r];
 #pragma unroll
     for (int j = 0; j < C_::NT; ++j) {
-      int r = wm * C_::WTM + i * 8 + g;
-      int c = wn * C_::WTN + j * 8 + 2 * t;
-      Cs[r * C_::LDC + c] = alpha * acc[i][j][0];
-      Cs[r * C_::LDC + c + 1] = alpha * acc[i][j][1];
-    }
-  __syncthreads();
-  double ss = 0.0;
-  if (args.c_nfast) {
-    for (int e = tid; e < BM * BN; e += THREADS) {
-      int nl = e % BN, ml = e / BN;
-      int mo = c_moff[ml], no = c_noff[nl];
-      if (mo >= 0 && no >= 0) {
-        double v = Cs[ml * C_::LDC + nl];
-        if (beta != 0.0) v += beta * Cg[mo + no];
-        Cg[mo + no] = v;
-        ss += v * v;
-      }
-    }
-  } else {
-    for (int e = tid; e < BM * BN; e += THREADS) {
-      int ml = e % BM, nl = e / BM;
-      int mo = c_moff[ml], no = c_noff[nl];
-      if (mo >= 0 && no >= 0) {
-        double v = Cs[ml * C_::LDC + nl];
-        if (beta != 0.0) v += beta * Cg[mo + no];
-        Cg[mo + no] = v;
-        ss += v * v;
+      const int c = wn * C_::WTN + j * 8 + 2 * t;
+      const int no0 = c_noff[c], no1 = c_noff[c + 1];
+      if (mo >= 0) {
+        if (no0 >= 0) {
+          double v = alpha * acc[i][j][0];
+          if (beta != 0.0) v += beta * Cg[mo + no0];
+          Cg[mo + no0] = v;
+          ss += v * v;
+        }
+        if (no1 >= 0) {
+          double v = alpha * acc[i][j][1];
+          if (beta != 0.0) v += beta * Cg[mo + no1];
+          Cg[mo + no1] = v;
+          ss += v * v;
+        }
       }
     }
   }
-  if (args.sumsq[bz] != nullptr) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (lane == 0) atomicAdd(args.sumsq[bz], ss);
-  }
+  if (args.sumsq[bz] != nullptr) block_sum_store(ss, args.sumsq[bz] + blockIdx.y * gridDim.x + blockIdx.x);
 }
 
 }  // namespace tc

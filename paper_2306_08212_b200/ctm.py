@@ -22,6 +22,7 @@ CTM_SEQUENTIAL = 0
 CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD = 0, 1, 2
 CTM_FLAG_CHECK_FINITE = 1
 CTM_FLAG_MOVE_ONLY = 2
+CTM_FLAG_PROFILE = 4
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
 DIRS = {"left": 0, "right": 1, "up": 2, "down": 3}
@@ -46,7 +47,8 @@ class ctm_env(ctypes.Structure):
 
 class ctm_move_stats(ctypes.Structure):
     _fields_ = [("ms_total", c_double), ("ms_svd", c_double), ("ms_contract", c_double), ("flops", c_double),
-                ("min_gap", c_double), ("n_svd", c_int), ("n_kernels", c_int)]
+                ("min_gap", c_double), ("n_svd", c_int), ("n_kernels", c_int), ("ms_gemm", c_double),
+                ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
