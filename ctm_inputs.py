@@ -66,7 +66,13 @@ CONFIGS = {
     "c4": Config("c4", 3, 2, 8, 128, 128, 128, True),
     "c5": Config("c5", 4, 2, 10, 200, 200, 200, True),
     "c5_256": Config("c5_256", 4, 2, 10, 256, 256, 256, True),
+    # converging variants (reading R16b): partial-trace start, chi = D^2 so every boundary
+    # extent equals chi from the first move; used for the 1e-9 gauge-invariant parity.
+    "c2_dl": Config("c2_dl", 1, 2, 4, 16, 16, 16, False),
+    "c3_dl": Config("c3_dl", 2, 2, 6, 36, 36, 36, True),
+    "c4_dl": Config("c4_dl", 3, 2, 8, 64, 64, 64, True),
 }
+ENV_INIT = {"c2_dl": "double_layer", "c3_dl": "double_layer", "c4_dl": "double_layer"}
 
 
 def custom(d: int, D: int, chi: int, *, chi_p: int | None = None, chi_pp: int | None = None,
@@ -85,8 +91,15 @@ def _site(rng: np.random.Generator, d: int, D: int, decaying: bool) -> np.ndarra
     return A / np.linalg.norm(A)
 
 
-def generate(cfg: Config) -> dict:
-    """Return {'A','B', 'C': {(x,k): arr}, 'T': {(x,k): arr}} in clockwise storage."""
+def generate(cfg: Config, env_init: str | None = None) -> dict:
+    """Return {'A','B', 'C': {(x,k): arr}, 'T': {(x,k): arr}} in clockwise storage.
+
+    env_init "gaussian" is BASELINE.json's recipe.  "double_layer" (DESIGN.md reading
+    R16b) replaces the boundary tensors by the standard partial-trace start of CTM
+    (trace the outward legs of the double-layer site), a positive
+    environment for which CTM converges smoothly; the same seeded A, B are used."""
+    if env_init is None:
+        env_init = ENV_INIT.get(cfg.name, "gaussian")
     rng = np.random.Generator(np.random.PCG64(cfg.seed))
     A = _site(rng, cfg.d, cfg.D, cfg.decaying)
     B = _site(rng, cfg.d, cfg.D, cfg.decaying)
@@ -101,7 +114,36 @@ def generate(cfg: Config) -> dict:
             t = rng.standard_normal((c0, cfg.D, cfg.D, c0))
             t = 0.5 * (t + t.swapaxes(1, 2))
             T[(x, k)] = t / np.linalg.norm(t)
+    if env_init == "double_layer":
+        C, T = _partial_trace_env(A, B)
+    elif env_init != "gaussian":
+        raise ValueError(env_init)
     return {"A": A, "B": B, "C": C, "T": T}
+
+
+def _partial_trace_env(A, B):
+    """Boundary from the double-layer sites with the outward legs traced (ket = bra),
+    boundary extent D^2 (grows to chi over the first moves).  Input preparation only:
+    the fused legs keep the clockwise storage order of the module docstring."""
+    D = A.shape[1]
+    D2 = D * D
+    site = {"a": A, "b": B}
+    C, T = {}, {}
+    for x, y in (("a", "b"), ("b", "a")):
+        ax = np.einsum("sabcd,sefgh->aebfcgdh", site[x], site[x])   # (uk,ub,lk,lb,dk,db,rk,rb)
+        ay = np.einsum("sabcd,sefgh->aebfcgdh", site[y], site[y])
+        # corners: the diagonal neighbour has x's sublattice; edges: the neighbour is y
+        C[(x, 1)] = np.einsum("aabbcdef->cdef", ax).reshape(D2, D2)          # (d, r)
+        C[(x, 2)] = np.einsum("aacdefbb->cdef", ax).reshape(D2, D2)          # (l, d)
+        C[(x, 3)] = np.einsum("cdefaabb->cdef", ax).reshape(D2, D2)          # (u, l)
+        C[(x, 4)] = np.einsum("cdaabbef->efcd", ax).reshape(D2, D2)          # (r, u)
+        T[(x, 1)] = np.einsum("uvaadekb->dekbuv", ay).reshape(D2, D, D, D2)  # (d, k, b, u)
+        T[(x, 2)] = np.einsum("aalmkbrs->lmkbrs", ay).reshape(D2, D, D, D2)  # (l, k, b, r)
+        T[(x, 3)] = np.einsum("uvkbdeaa->uvkbde", ay).reshape(D2, D, D, D2)  # (u, k, b, d)
+        T[(x, 4)] = np.einsum("kblmaars->rskblm", ay).reshape(D2, D, D, D2)  # (r, k, b, l)
+    C = {k: v / np.linalg.norm(v) for k, v in C.items()}
+    T = {k: v / np.linalg.norm(v) for k, v in T.items()}
+    return C, T
 
 
 def random_isometries(rng: np.random.Generator, chi: int, D: int, chi_p: int, chi_out: int):

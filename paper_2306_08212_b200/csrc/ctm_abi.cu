@@ -666,6 +666,59 @@ double norm_2x2_impl(Handle& h, const double* A, const double* B, const ctm_env*
   return v;
 }
 
+// Bond energy on the 2x1 window (A left of B), reading R18:
+//   C_a^1 T_a^2 T_b^2 C_b^2 / T_a^1 A B T_b^3 / C_a^4 T_a^4 T_b^4 C_b^3
+// rho(sA,sB,tA,tB) = L(Y,U,sA,r,tA,w) R(Y,U,sB,r,tB,w); ket then bra absorbed per half
+// (peak intermediate chi^2 d^2 D^4) so it also runs at C4 sizes.
+double bond_energy_impl(Handle& h, const double* A, const double* B, const ctm_env* env, const double* hop,
+                        double* rho_out) {
+  const int D = h.prm.D, d = h.prm.d;
+  const size_t mark = h.ws.top;
+  Ten sA{const_cast<double*>(A), {d, D, D, D, D}}, sB{const_cast<double*>(B), {d, D, D, D, D}};
+  const int a = 0, b = 1;
+  Ten c1 = envC(env, a, 1), t2 = envT(env, a, 2, D), t1 = envT(env, a, 1, D), c4 = envC(env, a, 4),
+      t4 = envT(env, a, 4, D);
+  // left half
+  Ten E1 = alloc(h, {c1.ext[0], D, D, t2.ext[3]});
+  contract(h, op({&c1}, "xy"), op({&t2}, "ymnY"), out({&E1}, "xmnY"));
+  Ten E2 = alloc(h, {D, D, t2.ext[3], t1.ext[0], D, D});
+  contract(h, op({&E1}, "xmnY"), op({&t1}, "Xkbx"), out({&E2}, "mnYXkb"));
+  Ten E3 = alloc(h, {D, t2.ext[3], t1.ext[0], D, d, D, D});
+  contract(h, op({&E2}, "mnYXkb"), op({&sA}, "smkpr"), out({&E3}, "nYXbspr"));
+  Ten E4 = alloc(h, {t2.ext[3], t1.ext[0], d, D, D, d, D, D});
+  contract(h, op({&E3}, "nYXbspr"), op({&sA}, "tnbqw"), out({&E4}, "YXsprtqw"));
+  Ten F1 = alloc(h, {c4.ext[1], t4.ext[0], D, D});
+  contract(h, op({&c4}, "ZX"), op({&t4}, "UpqZ"), out({&F1}, "XUpq"));
+  Ten L = alloc(h, {t2.ext[3], t4.ext[0], d, D, d, D});
+  contract(h, op({&E4}, "YXsprtqw"), op({&F1}, "XUpq"), out({&L}, "YUsrtw"));
+  // right half
+  Ten u2 = envT(env, b, 2, D), c2 = envC(env, b, 2), u3 = envT(env, b, 3, D), c3 = envC(env, b, 3),
+      u4 = envT(env, b, 4, D);
+  Ten G1 = alloc(h, {u2.ext[0], D, D, c2.ext[1]});
+  contract(h, op({&u2}, "Ymnz"), op({&c2}, "zc"), out({&G1}, "Ymnc"));
+  Ten G2 = alloc(h, {u2.ext[0], D, D, D, D, u3.ext[3]});
+  contract(h, op({&G1}, "Ymnc"), op({&u3}, "cklW"), out({&G2}, "YmnklW"));
+  Ten G3 = alloc(h, {u2.ext[0], D, D, u3.ext[3], d, D, D});
+  contract(h, op({&G2}, "YmnklW"), op({&sB}, "Smrpk"), out({&G3}, "YnlWSrp"));
+  Ten G4 = alloc(h, {u2.ext[0], u3.ext[3], d, D, D, d, D, D});
+  contract(h, op({&G3}, "YnlWSrp"), op({&sB}, "Tnwql"), out({&G4}, "YWSrpTwq"));
+  Ten H1 = alloc(h, {c3.ext[0], u4.ext[3], D, D});
+  contract(h, op({&c3}, "WV"), op({&u4}, "VpqU"), out({&H1}, "WUpq"));
+  Ten R = alloc(h, {u2.ext[0], u4.ext[3], d, D, d, D});
+  contract(h, op({&G4}, "YWSrpTwq"), op({&H1}, "WUpq"), out({&R}, "YUSrTw"));
+  Ten rho = alloc(h, {d, d, d, d});
+  contract(h, op({&L}, "YUsrtw"), op({&R}, "YUSrTw"), out({&rho}, "sStT"));
+  double* e_dev = h.ws.take(1);
+  rho_finish(h, rho.p, hop, d, rho_out, e_dev);
+  double e = 0.0;
+  if (!h.dry) {
+    CTM_CUDA(cudaMemcpyAsync(&e, e_dev, sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+  }
+  h.ws.reset(mark);
+  return e;
+}
+
 }  // namespace
 }  // namespace ctm
 
@@ -783,6 +836,12 @@ void size_workspace(Handle& h) {
     h.ws.reset(0);
     h.ws.peak = 0;
     ctm::norm_2x2_impl(h, dummy, dummy, &env, true);
+    main_need = std::max(main_need, h.ws.peak);
+    h.ws.reset(0);
+    h.ws.peak = 0;
+    const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D;
+    h.ws.take(2 * ns);
+    ctm::bond_energy_impl(h, dummy, dummy, &env, dummy, nullptr);
     main_need = std::max(main_need, h.ws.peak);
   }
   set_dry(h, false);
@@ -1048,8 +1107,23 @@ int ctm_norm_2x2(ctm_handle hh, const double* A, const double* B, const ctm_env*
 int ctm_bond_energy(ctm_handle hh, const double* A, const double* B, const ctm_env* env, const double* hop,
                     int bond, double* rho_out, double* e_out_host) {
   return guarded(hh, [&](Handle& h) {
-    (void)A; (void)B; (void)env; (void)hop; (void)bond; (void)rho_out; (void)e_out_host;
-    throw Error(CTM_E_UNSUPPORTED, "ctm_bond_energy: not built yet");
+    if (!A || !B || !env || !hop || !e_out_host || (bond != CTM_BOND_H && bond != CTM_BOND_V))
+      throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    if (bond == CTM_BOND_H) {
+      *e_out_host = ctm::bond_energy_impl(h, A, B, env, hop, rho_out);
+    } else {
+      // A above B: one counter-clockwise quarter turn (= 3 clockwise) brings it to A left of B
+      const size_t ns = (size_t)h.prm.d * h.prm.D * h.prm.D * h.prm.D * h.prm.D;
+      double* Ar = h.ws.take(ns);
+      double* Br = h.ws.take(ns);
+      ctm::rotate_site(h, A, Ar, 3);
+      ctm::rotate_site(h, B, Br, 3);
+      ctm_env e = *env;
+      for (int i = 0; i < 3; ++i) ctm::rotate_env_cw(&e);
+      *e_out_host = ctm::bond_energy_impl(h, Ar, Br, &e, hop, rho_out);
+    }
   });
 }
 

@@ -111,6 +111,8 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
 void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count);
 void abs_copy(Handle& h, const double* src, double* dst, size_t n);
 void dot(Handle& h, const double* a, const double* b, size_t n, double* out);   // out = a.b (device)
+// rho (d,d,d,d) -> symmetrised, trace-normalised; e = Tr(rho h) into e_dev; rho_out nullable
+void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* rho_out, double* e_dev);
 
 // svd.cu: first n_keep left singular vectors of the row-major R x C matrix `mat`
 // (input preserved), written row-major (R, n_keep) with the sign rule.  Returns the

@@ -118,6 +118,28 @@ __global__ void dot_kernel(const double* __restrict__ a, const double* __restric
   }
 }
 
+// One block: m = (rho + rho^T)/2 as (sA sB) x (tA tB); m /= Tr m; e = sum_ij m_ij h_ji.
+__global__ void rho_finish_kernel(const double* __restrict__ rho, const double* __restrict__ hop, int n,
+                                  double* __restrict__ rho_out, double* __restrict__ e_out) {
+  __shared__ double tr;
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < n; ++i) t += rho[i * n + i];
+    tr = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double e = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        const double m = 0.5 * (rho[i * n + j] + rho[j * n + i]) / tr;
+        e += m * hop[j * n + i];
+        if (rho_out) rho_out[i * n + j] = m;
+      }
+    *e_out = e;
+  }
+}
+
 int grid_for(long long n, int threads = 256) {
   long long b = (n + threads - 1) / threads;
   long long cap = kSMs * 8;
@@ -193,6 +215,13 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
 void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count) {
   if (h.dry) return;
   nonfinite_kernel<<<grid_for((long long)n), 256, 0, h.stream>>>(p, (long long)n, dev_count);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* rho_out, double* e_dev) {
+  if (h.dry) return;
+  rho_finish_kernel<<<1, 32, 0, h.stream>>>(rho, hop, d * d, rho_out, e_dev);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
