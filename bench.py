@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--svd", default="gesvdp", choices=["gesvdp", "gesvdj", "gesvd"])
+    ap.add_argument("--svd", default="iso", choices=["gesvdp", "gesvdj", "gesvd", "gram", "iso"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -150,7 +150,7 @@ def bench_ours(args, cfg):
     dev = torch.device(f"cuda:{local}")
     torch.cuda.set_device(dev)
     from paper_2306_08212_b200 import ctm
-    svd = {"gesvdp": ctm.CTM_SVD_GESVDP, "gesvdj": ctm.CTM_SVD_GESVDJ, "gesvd": ctm.CTM_SVD_GESVD}[args.svd]
+    svd = {"gesvdp": ctm.CTM_SVD_GESVDP, "gesvdj": ctm.CTM_SVD_GESVDJ, "gesvd": ctm.CTM_SVD_GESVD, "gram": ctm.CTM_SVD_GRAM, "iso": ctm.CTM_SVD_ISO}[args.svd]
     stream = torch.cuda.Stream(dev)
     g = ci.generate(cfg)
     with torch.cuda.stream(stream):
@@ -254,6 +254,7 @@ def bench_ours(args, cfg):
                    "D": cfg.D, "chi": cfg.chi, "parallelism": f"replicas{world}",
                    "l2": "256 MB L2 flush between timed steps; intermediates > L2"},
         "ms_isometry_stage_per_move": ms_iso, "ms_svd_calls_summed_per_move": ms_svd,
+        "svd_fallbacks_per_move": float(np.mean([s.get("n_svd_fallback", 0) for s in stats])),
         "ms_absorb_per_move": t_step - ms_iso,
         "contraction_only": {"moves_per_s": world * 1e3 / t_c, "ms_per_move": t_c,
                              "flops_per_move": gem_fl, "tflops": gem_fl / (t_c * 1e-3) / 1e12,

@@ -63,9 +63,20 @@ extern "C" {
 #define CTM_REDUCED_EXACT 1  /* NEXT on the GPU (oracle only in round 1)               */
 
 /* SVD back-ends (ctm_params.svd_algo); all on the device, no CPU fallback */
-#define CTM_SVD_GESVDP 0     /* cuSOLVER Xgesvdp (polar decomposition), default       */
+#define CTM_SVD_GESVDP 0     /* cuSOLVER Xgesvdp (polar decomposition)                */
 #define CTM_SVD_GESVDJ 1     /* cuSOLVER gesvdj (Jacobi), tolerance svd_tol            */
 #define CTM_SVD_GESVD 2      /* cuSOLVER Xgesvd (QR iteration)                         */
+#define CTM_SVD_GRAM 3       /* truncating cuts (n_keep < rows <= cols): top eigenvectors of
+                                the Gram matrix M M^T (libctm DMMA GEMM + cuSOLVER syevd);
+                                every other shape: Xgesvdp.  Subspace error
+                                ~ eps (s_1/s_n)^2 / (1 - (s_{n+1}/s_n)^2) instead of
+                                eps (s_1/s_n) / (1 - s_{n+1}/s_n).          */
+#define CTM_SVD_ISO 4        /* libctm's own solver (default): subspace iteration on M M^T
+                                with CholQR, Rayleigh-Ritz through a backward-stable QR and
+                                one-sided Jacobi (all libctm kernels + DMMA GEMMs); tall /
+                                small cuts: QR + one-sided Jacobi.  Shapes beyond its
+                                shared-memory limit (l > 160) or whose convergence it cannot
+                                certify fall back to Xgesvdp (counted in n_svd_fallback). */
 
 /* flags (ctm_params.flags) */
 #define CTM_FLAG_CHECK_FINITE 1   /* scan every committed tensor for NaN/Inf         */
@@ -128,6 +139,7 @@ typedef struct {
   int gemm_launches;    /* number of tc_gemm launches                                  */
   double ms_isometry;   /* wall device time of the isometry stages (reduced envs + TS,  */
                         /* rows a1-a5) on the caller's stream, fork to join            */
+  int n_svd_fallback;   /* CTM_SVD_ISO truncations that fell back to cuSOLVER Xgesvdp   */
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by

@@ -287,6 +287,7 @@ void sub_begin(Handle& s) {
   s.flops = 0.0;
   s.min_gap = std::numeric_limits<double>::infinity();
   s.n_svd = 0;
+  s.n_svd_fallback = 0;
   s.n_kernels = 0;
   s.dry = false;
 }
@@ -295,6 +296,7 @@ void sub_merge(Handle& h, Handle& s) {
   h.flops += s.flops;
   h.min_gap = std::min(h.min_gap, s.min_gap);
   h.n_svd += s.n_svd;
+  h.n_svd_fallback += s.n_svd_fallback;
   h.n_kernels += s.n_kernels;
   h.kernel_count += s.n_kernels;
 }
@@ -761,6 +763,7 @@ void begin_call(Handle& h) {
   h.flops = 0.0;
   h.min_gap = std::numeric_limits<double>::infinity();
   h.n_svd = 0;
+  h.n_svd_fallback = 0;
   h.n_kernels = 0;
   h.prof_used = 0;
   if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
@@ -776,6 +779,7 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->flops = h.flops;
   st->min_gap = h.min_gap;
   st->n_svd = h.n_svd;
+  st->n_svd_fallback = h.n_svd_fallback;
   st->n_kernels = h.n_kernels;
   st->ms_gemm = 0.0;
   st->gemm_flops = 0.0;
@@ -860,6 +864,7 @@ void init_solver(Handle& h, const ctm_params* p) {
   cusolverDnXgesvdjSetTolerance(h.gesvdj_info, tol);
   cusolverDnXgesvdjSetMaxSweeps(h.gesvdj_info, 100);
   cusolverDnSetStream(h.solver, h.stream);
+  ctm::iso_init_kernels();
   CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
   h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
   for (auto& e : h.ev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));

@@ -69,7 +69,7 @@ struct Handle {
   std::vector<char> host_buf;          // cuSOLVER host workspace
   int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
   double* dev_scalars = nullptr;        // small device scratch (norms etc.)
-  cudaEvent_t ev[6]{};
+  cudaEvent_t ev[8]{};   // 2,3: svd timing; 4,5: isometry fork/join; 6,7: iso solver debug
   std::string last_error;
   int64_t kernel_count = 0;
   // per-call statistics
@@ -78,6 +78,7 @@ struct Handle {
   double flops = 0.0;
   double min_gap = 1e300;
   int n_svd = 0;
+  int n_svd_fallback = 0;               // CTM_SVD_ISO truncations handed to cuSOLVER
   int n_kernels = 0;
   bool dry = false;                     // sizing pass: no launches
   // CTM_FLAG_PROFILE: event pairs around each tc_gemm launch
@@ -118,6 +119,14 @@ void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* 
 // (input preserved), written row-major (R, n_keep) with the sign rule.  Returns the
 // truncation gap sigma_{n}/sigma_{n+1} (inf if none).
 double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out);
+
+// iso.cu: libctm's own truncated SVD (subspace iteration + CholQR + one-sided Jacobi).
+#define CTM_ISO_LMAX 160
+void iso_init_kernels();
+bool iso_supported(int R, int C, int n_keep);
+// ok = false when convergence could not be certified (caller falls back to cuSOLVER).
+double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
+                        void (*signfix)(Handle&, const double*, long long, long long, int, int, double*), bool* ok);
 size_t svd_workspace_doubles(Handle& h, int R, int C);
 
 }  // namespace ctm

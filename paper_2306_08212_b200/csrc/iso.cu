@@ -1,0 +1,392 @@
+// iso.cu -- libctm's own truncated-SVD solver for the isometries (
+// P:L46 "the unitary matrix U is reshaped ... truncation applied corresponding to the
+// largest chi singular values", P:L60 two-stage recipe; north star: "cuSOLVER gesvdj or a
+// hand-written Jacobi kernel").
+//
+// What the paper needs from an SVD here is the first n left singular vectors of an R x C
+// matrix M (R = chi D, n = chi' = R / D): a small slice of the spectrum.  Dense cuSOLVER
+// factorisations of 1024^2 are latency bound (35-95 ms, profiles/r01_probe_svd.txt), so
+// libctm computes only that slice:
+//
+//  * truncating cut (n < R):  subspace iteration on M M^T with a block of l = n + p columns
+//      Y <- orth(M (M^T Y)),  orth = CholQR (Gram on the DMMA GEMM, one-CTA Cholesky,
+//      row-parallel triangular solve), then a Rayleigh-Ritz step that never forms a Gram
+//      of M: Z = M^T Y = Q_z R_z (shifted CholQR3, backward stable), the left singular
+//      vectors W of R_z^T by one-sided Jacobi in shared memory, U = Y W.  Convergence is
+//      certified by the residuals ||M M^T u_i - s_i^2 u_i|| of the kept Ritz vectors.
+//  * non-truncating / tall cut (stage two of TS, n >= C):  M = Q_o R (shifted CholQR3),
+//      U = Q_o * lsv(R) with lsv(R) by the same one-sided Jacobi kernel.
+//
+// Accuracy: the Rayleigh-Ritz and the tall path are backward stable in M (no squared
+// condition number, unlike a Gram eigensolver, which failed c3_dl's conditioning test);
+// subspace iteration adds a containment error that the residual test drives to the
+// rounding floor.  The sign rule (largest-|.| entry of each column positive) is applied by
+// the same extraction kernel the cuSOLVER path uses.
+//
+// Shapes this solver does not take (l > CTM_ISO_LMAX, or a rank-deficient keep with
+// n > C) go to cuSOLVER gesvdp (svd.cu); there is no CPU path.
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <limits>
+#include <vector>
+
+#include "ctm_internal.h"
+#include "iso_kernels.cuh"
+
+namespace ctm {
+namespace {
+
+using namespace isok;
+constexpr int ISO_OVERSAMPLE = 32;
+constexpr double EPS = 2.220446049250313e-16;
+
+// ---------------------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------------------
+struct IsoFail : std::runtime_error {
+  explicit IsoFail(const std::string& m) : std::runtime_error(m) {}
+};
+
+void set_smem(const void* f, size_t bytes) {
+  CTM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+struct Solver {
+  Handle& h;
+  int* status;   // device: [0] CholQR pivot, [1] Jacobi failure, [2] Jacobi sweeps
+  int last_sweeps = 0;
+  int* repl;     // device: per-column "numerically dependent" flags (chol_kernel)
+  unsigned seed = 0x9e3779b9u;
+  explicit Solver(Handle& hh) : h(hh) {
+    status = reinterpret_cast<int*>(h.ws.take(8));
+    repl = reinterpret_cast<int*>(h.ws.take(LMAX / 2 + 1));
+    if (!h.dry) {
+      CTM_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(double), h.stream));
+      CTM_CUDA(cudaMemsetAsync(repl, 0, LMAX * sizeof(int), h.stream));
+    }
+  }
+  // C (m x n) = A * B with row-major operands given by label strings.
+  void gemm(const double* A, const char* la, std::vector<int> ea, const double* B, const char* lb,
+            std::vector<int> eb, double* C, const char* lc, std::vector<int> ec) {
+    Operand a{{A}, la, ea}, b{{B}, lb, eb};
+    OutOperand c{{C}, lc, ec, {}};
+    const double f = h.flops;
+    contract(h, a, b, c);
+    h.flops = f;   // solver work is not part of the move's algorithmic flops (R21)
+  }
+  // One CholQR pass on Y (m x n): S = Y^T Y, S (+shift) = R^T R, Y <- Y R^{-1}.
+  // replace: numerically dependent columns (pivot <= 1e-13 of the column's squared norm)
+  // are overwritten with random directions instead of failing; a later pass re-orthonormalises.
+  void cholqr_pass(double* Y, int m, int n, double shift_factor, double* R, bool replace = false) {
+    const size_t mark = h.ws.top;
+    double* S = h.ws.take((size_t)n * n);
+    double* rd = h.ws.take((size_t)n);
+    gemm(Y, "ia", {m, n}, Y, "ib", {m, n}, S, "ab", {n, n});
+    if (h.dry) {
+      h.ws.reset(mark);
+      return;
+    }
+    const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
+    chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
+                                                          replace ? repl : nullptr);
+    CTM_CUDA(cudaGetLastError());
+    const int rows_per_cta = 8;
+    const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
+    trsm_rows_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel(2);
+    if (replace) {
+      replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
+      CTM_CUDA(cudaGetLastError());
+      h.count_kernel();
+    }
+    h.ws.reset(mark);
+  }
+  // passes of CholQR (the first one shifted when `shifted`), R_total = R_p ... R_1.
+  void cholqr(double* Y, int m, int n, int passes, bool shifted, double* Rtot, bool replace = false) {
+    const size_t mark = h.ws.top;
+    double* R = h.ws.take((size_t)n * n);
+    double* T = Rtot ? h.ws.take((size_t)n * n) : nullptr;
+    for (int p = 0; p < passes; ++p) {
+      const double sf = (shifted && p == 0) ? 11.0 * ((double)m * n + (double)n * (n + 1)) * EPS : 0.0;
+      double* Rp = (Rtot && p == 0) ? Rtot : R;
+      cholqr_pass(Y, m, n, sf, Rp, replace && p == 1);   // the first plain pass may replace columns
+      if (Rtot && p > 0) {   // Rtot <- R_p Rtot
+        gemm(R, "ab", {n, n}, Rtot, "bc", {n, n}, T, "ac", {n, n});
+        if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Rtot, T, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, h.stream));
+      }
+    }
+    h.ws.reset(mark);   // stream order makes the scratch reusable by the next call
+  }
+  void jacobi(const double* X, int n, int trans, int ncols, double* U, double* S, double tol = 1e-14) {
+    if (h.dry) return;
+    const size_t smem = (size_t)n * n * sizeof(double);
+    jacobi_lsv_kernel<<<1, 1024, smem, h.stream>>>(X, n, trans, ncols, U, S, status + 1, 60, tol);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+  }
+  void check_status(const char* what) {
+    if (h.dry) return;
+    int st[3] = {0, 0, 0};
+    CTM_CUDA(cudaMemcpyAsync(st, status, sizeof(st), cudaMemcpyDeviceToHost, h.stream));
+    last_sweeps = st[2];
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    if (st[0] != 0) throw IsoFail(std::string(what) + ": CholQR pivot " + std::to_string(st[0]) + " not positive");
+    if (st[1] != 0) throw IsoFail(std::string(what) + ": Jacobi did not converge");
+  }
+};
+
+}  // namespace
+
+void iso_init_kernels() {
+  static bool done = false;
+  if (done) return;
+  const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
+  set_smem((const void*)chol_kernel, big);
+  set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * LMAX * sizeof(double));
+  done = true;
+}
+
+// Which path takes an R x C truncation to n_keep columns: 0 none (cuSOLVER), 1 direct tall
+// (R > C), 2 direct wide (R <= C, R small or no truncation), 3 subspace iteration.
+static int iso_plan(int R, int C, int n_keep) {
+  if (R > C) return (n_keep <= C && C <= LMAX) ? 1 : 0;   // n_keep > C: R11 null-space columns
+  if (n_keep == R || R <= n_keep + ISO_OVERSAMPLE) return R <= LMAX ? 2 : 0;
+  return n_keep + ISO_OVERSAMPLE <= LMAX ? 3 : 0;
+}
+
+bool iso_supported(int R, int C, int n_keep) { return iso_plan(R, C, n_keep) != 0; }
+
+// First n_keep left singular vectors of the row-major R x C matrix `mat` (sign rule
+// applied), written row-major (R, n_keep) into `out`.  Returns sigma_n / sigma_{n+1}
+// (inf if none).  Throws IsoFail when the iteration cannot certify convergence.
+static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
+                       void (*signfix)(Handle&, const double*, long long, long long, int, int, double*)) {
+  const size_t mark = h.ws.top;
+  Solver sv(h);
+  const double inf = std::numeric_limits<double>::infinity();
+  double gap = inf;
+  const int plan = iso_plan(R, C, n_keep);
+  if (plan == 1 || plan == 2) {
+    // direct: left singular vectors from a backward-stable QR + one-sided Jacobi
+    //   tall (R >= C):  M = Q_o R_m,        U = Q_o lsv(R_m)
+    //   wide (R <= C):  M^T = Q_z R_z,      U = lsv(R_z^T)
+    const bool tall = plan == 1;
+    const int n = tall ? C : R;
+    double* Y = h.ws.take((size_t)R * C);
+    double* Rm = h.ws.take((size_t)n * n);
+    double* W = h.ws.take((size_t)n * n);
+    double* S = h.ws.take((size_t)n);
+    double* Ut = tall ? h.ws.take((size_t)R * n) : nullptr;
+    if (!h.dry) {
+      if (tall) CTM_CUDA(cudaMemcpyAsync(Y, mat, sizeof(double) * R * C, cudaMemcpyDeviceToDevice, h.stream));
+      else permute(h, mat, {R, C}, {1, 0}, Y);   // M^T (C x R)
+    }
+    sv.cholqr(Y, tall ? R : C, n, 3, true, Rm);
+    sv.jacobi(Rm, n, tall ? 0 : 1, n, W, S);
+    ++h.n_svd;
+    if (h.dry) {
+      h.ws.reset(mark);
+      return inf;
+    }
+    const double* U = W;
+    if (tall) {
+      sv.gemm(Y, "ia", {R, n}, W, "ab", {n, n}, Ut, "ib", {R, n});
+      U = Ut;
+    }
+    signfix(h, U, n, 1, R, n_keep, out);
+    sv.check_status("iso direct");
+    std::vector<double> s(n);
+    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    for (double x : s)
+      if (!std::isfinite(x)) throw Error(CTM_E_NONFINITE, "non-finite singular value in a " + std::to_string(R) +
+                                                               " x " + std::to_string(C) + " isometry");
+    if (n_keep < n && s[n_keep] > 0.0) gap = s[n_keep - 1] / s[n_keep];
+    h.ws.reset(mark);
+    return gap;
+  }
+  // truncating cut: Chebyshev-filtered subspace iteration with Rayleigh-Ritz
+  const int l = std::min(n_keep + ISO_OVERSAMPLE, R);
+  const int k = n_keep;
+  double* Y = h.ws.take((size_t)R * l);
+  double* Y1 = h.ws.take((size_t)R * l);
+  double* Y2 = h.ws.take((size_t)R * l);
+  double* P = h.ws.take((size_t)R * l);
+  double* Z = h.ws.take((size_t)C * l);
+  double* Rz = h.ws.take((size_t)l * l);
+  double* W = h.ws.take((size_t)l * l);
+  double* S = h.ws.take((size_t)l);
+  double* U = h.ws.take((size_t)R * l);
+  double* PW = h.ws.take((size_t)R * l);
+  double* res = h.ws.take((size_t)l);
+  ++h.n_svd;
+  static const bool debug = std::getenv("CTM_ISO_DEBUG") != nullptr;
+  cudaEvent_t t0 = h.ev[2];
+  float ms_rr = 0.f, ms_all = 0.f;
+  auto GY = [&](const double* X, double* out) {   // out = M M^T X; leaves M^T X in Z
+    sv.gemm(mat, "ic", {R, C}, X, "ia", {R, l}, Z, "ca", {C, l});
+    sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, out, "ia", {R, l});
+  };
+  // Filter products through G = M M^T (one GEMM per degree instead of two) when the
+  // kept spectrum is flat: the containment floor of the G-form is ~ eps (s_1/s_k)^2,
+  // allowed only while that is <= 16 eps.  The Rayleigh-Ritz always uses M itself.
+  double* G = h.ws.take((size_t)R * R);
+  bool have_G = false;
+  auto GYf = [&](const double* X, double* out) {
+    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, l}, out, "ia", {R, l});
+    else GY(X, out);
+  };
+  auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c) {
+    if (h.dry) return;
+    cheb_combine_kernel<<<148, 256, 0, h.stream>>>(out, Pm, Yc, Yo, (long long)R * l, a, b2, c);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+  };
+  // start: Y = orth(M Omega), then two plain steps Y <- orth(M M^T Y)
+  if (!h.dry) {
+    fill_omega_kernel<<<148, 256, 0, h.stream>>>(Z, (long long)C * l, 0x5eed1234u);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+  }
+  sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
+  sv.cholqr(Y, R, l, 1, true, nullptr);
+  for (int it = 0; it < 4; ++it) {
+    GY(Y, P);
+    std::swap(Y, P);
+    sv.cholqr(Y, R, l, 1, true, nullptr);
+  }
+  std::vector<double> s(l), r(k);
+  double prev_worst = inf;
+  bool extrapolated = false;
+  int degrees = 4, checks = 0;
+  const int max_degrees = 400;
+  for (;;) {
+    ++checks;
+    // Rayleigh-Ritz on an orthonormal Y: Z = M^T Y, P = M Z, Z = Q_z R_z, W = lsv(R_z^T)
+    cudaEvent_t e_rr0 = h.ev[6], e_rr1 = h.ev[7];
+    if (!h.dry && debug) CTM_CUDA(cudaEventRecord(e_rr0, h.stream));
+    sv.cholqr(Y, R, l, 3, true, nullptr, true);   // sCholQR3 (dependent columns replaced): orthonormal
+    GY(Y, P);
+    sv.cholqr(Z, C, l, 3, true, Rz);         // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR3)
+    // the first Rayleigh-Ritz only estimates the spectrum for the filter: loose Jacobi
+    sv.jacobi(Rz, l, 1, l, W, S, checks == 1 ? 1e-8 : 1e-14);
+    sv.gemm(Y, "ia", {R, l}, W, "ab", {l, l}, U, "ib", {R, l});
+    sv.gemm(P, "ia", {R, l}, W, "ab", {l, l}, PW, "ib", {R, l});
+    if (h.dry) {   // sizing pass: also reserve the G-form GEMMs' split-K slabs
+      sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
+      sv.gemm(G, "ij", {R, R}, Y, "ja", {R, l}, P, "ia", {R, l});
+      h.ws.reset(mark);
+      return inf;
+    }
+    ritz_residual_kernel<<<k, 256, 0, h.stream>>>(PW, U, S, R, l, k, res);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+    if (debug) CTM_CUDA(cudaEventRecord(e_rr1, h.stream));
+    sv.check_status("iso subspace");
+    if (debug) std::fprintf(stderr, "[iso]   check %d after %d degrees: jacobi sweeps %d\n", checks, degrees, sv.last_sweeps);
+    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * l, cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaMemcpyAsync(r.data(), res, sizeof(double) * k, cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    if (debug) {
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, e_rr0, e_rr1));
+      ms_rr += ms;
+    }
+    // r_i / s_i^2 estimates how much of the true u_i lies outside span(Y); r_i itself
+    // cannot be measured below ~ eps sqrt(C) s_1^2 (rounding in M M^T Y).
+    double worst = 0.0, worst_abs = 0.0;
+    for (int i = 0; i < k; ++i) {
+      if (!std::isfinite(r[i]) || !std::isfinite(s[i]))
+        throw Error(CTM_E_NONFINITE, "non-finite Ritz value in a " + std::to_string(R) + " x " + std::to_string(C) +
+                                         " isometry");
+      worst = std::max(worst, s[i] > 0.0 ? r[i] / (s[i] * s[i]) : 0.0);
+      worst_abs = std::max(worst_abs, r[i]);
+    }
+    const double floor_abs = 64.0 * EPS * std::sqrt((double)C) * s[0] * s[0];
+    if (worst_abs <= floor_abs && extrapolated) break;   // at the rounding floor after the predicted steps
+    if (degrees >= max_degrees || worst > 0.5 * prev_worst)
+      throw IsoFail("subspace iteration did not converge: residual " + std::to_string(worst));
+    prev_worst = worst;
+    // Chebyshev filter (Zhou & Saad's scaled recurrence) damping [0, b], b = s_l^2 (the
+    // smallest Ritz value of the block), normalised at the k-th Ritz value; the error of
+    // the slowest kept vector shrinks by x_k + sqrt(x_k^2 - 1) per degree.
+    const double lk = s[k - 1] * s[k - 1], lb = s[l - 1] * s[l - 1], l1 = s[0] * s[0];
+    if (!have_G && l1 <= 16.0 * lk) {
+      sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
+      have_G = true;
+    }
+    if (!(lb < 0.999 * lk)) throw IsoFail("no spectral separation inside the block");
+    const double ce = 0.5 * lb;                       // centre = half width of [0, b]
+    const double xk = (lk - ce) / ce, x1 = (l1 - ce) / ce;
+    const double rate = xk + std::sqrt(xk * xk - 1.0);
+    int need = (int)std::ceil(1.25 * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
+    need = std::max(2, std::min(need, max_degrees - degrees));
+    // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
+    // (1e8 let the bottom columns of the block collapse numerically onto the top ones)
+    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(1e6) / (std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12))));
+    // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
+    // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
+    CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
+    int done = 0;
+    while (done < need) {
+      const int m = std::min(mb, need - done);
+      const double s1 = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
+      double sig = s1;
+      double *Yo = nullptr, *Yc = Y;
+      double* bufs[2] = {Y1, Y2};
+      int nb = 0;
+      for (int j = 0; j < m; ++j) {
+        GYf(Yc, P);
+        double* Yn = bufs[nb];
+        nb ^= 1;
+        if (j == 0) {
+          combine(Yn, P, Yc, nullptr, s1 / ce, -s1, 0.0);
+        } else {
+          const double sn = 1.0 / (2.0 / s1 - sig);
+          combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn);
+          sig = sn;
+        }
+        Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
+        Yc = Yn;
+      }
+      if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
+      sv.cholqr(Y, R, l, 1, true, nullptr);   // shifted: a basis is enough between filter blocks
+      done += m;
+    }
+    degrees += need;
+    extrapolated = true;
+  }
+  if (debug) {
+    CTM_CUDA(cudaEventRecord(h.ev[3], h.stream));
+    CTM_CUDA(cudaEventSynchronize(h.ev[3]));
+    CTM_CUDA(cudaEventElapsedTime(&ms_all, t0, h.ev[3]));
+  }
+  signfix(h, U, l, 1, R, n_keep, out);
+  if (k < l && s[k] > 0.0) gap = s[k - 1] / s[k];
+  if (debug)
+    std::fprintf(stderr, "[iso] %d x %d keep %d: l=%d degrees=%d checks=%d s1/sk=%.3g sl/sk=%.3g gap=%.5f ms=%.2f rr_ms=%.2f last_sweeps=%d\n",
+                 R, C, n_keep, l, degrees, checks, s[0] / s[k - 1], s[l - 1] / s[k - 1], gap, ms_all, ms_rr, sv.last_sweeps);
+  h.ws.reset(mark);
+  return gap;
+}
+
+double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
+                        void (*signfix)(Handle&, const double*, long long, long long, int, int, double*), bool* ok) {
+  *ok = true;
+  const size_t mark = h.ws.top;
+  const int n_svd = h.n_svd;
+  try {
+    return iso_left(h, mat, R, C, n_keep, out, signfix);
+  } catch (const IsoFail& e) {
+    static const bool debug = std::getenv("CTM_ISO_DEBUG") != nullptr;
+    if (debug) std::fprintf(stderr, "[iso] %d x %d keep %d: fallback (%s)\n", R, C, n_keep, e.what());
+    h.ws.reset(mark);
+    h.n_svd = n_svd;
+    *ok = false;
+    return std::numeric_limits<double>::infinity();
+  }
+}
+
+}  // namespace ctm

@@ -125,10 +125,99 @@ size_t query_lwork_bytes(Handle& h, const Plan& p, double* A, double* S, double*
   return dws;
 }
 
+void signfix_launch(Handle& h, const double* base, long long rs, long long cs, int R, int n_keep, double* out) {
+  extract_signfix_kernel<<<n_keep, 256, 0, h.stream>>>(base, rs, cs, R, n_keep, out);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+bool use_gram(const Handle& h, int R, int C, int n_keep) {
+  return h.prm.svd_algo == CTM_SVD_GRAM && n_keep < R && R <= C;
+}
+
+size_t gram_lwork_bytes(Handle& h, int R, double* G, double* W) {
+  size_t dws = 0, hws = 0;
+  CTM_SOLVER(cusolverDnXsyevd_bufferSize(h.solver, h.solver_params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R,
+                                         CUDA_R_64F, G, R, CUDA_R_64F, W, CUDA_R_64F, &dws, &hws));
+  if (h.host_buf.size() < hws + 16) h.host_buf.resize(hws + 16);
+  return dws;
+}
+
+// Truncating cut through the Gram matrix: G = M M^T (R x R, DMMA GEMM), eigenvectors by
+// cuSOLVER syevd (ascending), the last n_keep columns reversed are the first n_keep left
+// singular vectors of M (sigma_i = sqrt(lambda_i)).
+double svd_left_gram(Handle& h, const double* mat, int R, int C, int n_keep, double* out) {
+  const size_t mark = h.ws.top;
+  double* G = h.ws.take((size_t)R * R);
+  double* W = h.ws.take((size_t)R);
+  size_t lw_bytes = gram_lwork_bytes(h, R, G, W);
+  double* work = h.ws.take(lw_bytes / sizeof(double) + 1);
+  ++h.n_svd;
+  Operand a{{mat}, "ic", {R, C}}, b{{mat}, "jc", {R, C}};
+  OutOperand g{{G}, "ij", {R, R}, {}};
+  if (h.dry) {
+    const double flops_before = h.flops;
+    contract(h, a, b, g);   // sizing pass: reserves the split-K slab
+    h.flops = flops_before;
+    h.ws.reset(mark);
+    return std::numeric_limits<double>::infinity();
+  }
+  CTM_CUDA(cudaEventRecord(h.ev[2], h.stream));
+  const double flops_before = h.flops;   // the Gram GEMM is solver work, not move flops (R21)
+  contract(h, a, b, g);
+  h.flops = flops_before;
+  CTM_SOLVER(cusolverDnXsyevd(h.solver, h.solver_params, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, R,
+                              CUDA_R_64F, G, R, CUDA_R_64F, W, CUDA_R_64F, work, lw_bytes, h.host_buf.data(),
+                              h.host_buf.size(), h.dev_info));
+  // column R-1-j of the (symmetric, so layout-free) eigenvector matrix is kept column j
+  extract_signfix_kernel<<<n_keep, 256, 0, h.stream>>>(G + (size_t)(R - 1) * R, 1, -(long long)R, R, n_keep, out);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+  CTM_CUDA(cudaEventRecord(h.ev[3], h.stream));
+  int info = 0;
+  std::vector<double> lam(R);
+  CTM_CUDA(cudaMemcpyAsync(&info, h.dev_info, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+  CTM_CUDA(cudaMemcpyAsync(lam.data(), W, sizeof(double) * R, cudaMemcpyDeviceToHost, h.stream));
+  CTM_CUDA(cudaStreamSynchronize(h.stream));
+  float ms = 0.f;
+  CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[2], h.ev[3]));
+  h.ms_svd += ms;
+  if (info != 0)
+    throw Error(CTM_E_SOLVER, "Gram eigensolver did not converge (info=" + std::to_string(info) + ") for a " +
+                                  std::to_string(R) + " x " + std::to_string(C) + " matrix");
+  for (double x : lam)
+    if (!std::isfinite(x))
+      throw Error(CTM_E_NONFINITE, "non-finite Gram eigenvalue in a " + std::to_string(R) + " x " +
+                                       std::to_string(C) + " truncation");
+  h.ws.reset(mark);
+  const double lk = lam[R - n_keep], lk1 = lam[R - n_keep - 1];
+  double gap = lk1 > 0.0 ? std::sqrt(std::max(lk, 0.0) / lk1) : std::numeric_limits<double>::infinity();
+  if (gap < h.min_gap) h.min_gap = gap;
+  return gap;
+}
+
 }  // namespace
 
 double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out) {
   if (n_keep < 1 || n_keep > R) throw Error(CTM_E_ARG, "svd_left: n_keep out of range");
+  if (use_gram(h, R, C, n_keep)) return svd_left_gram(h, mat, R, C, n_keep, out);
+  if (h.prm.svd_algo == CTM_SVD_ISO && iso_supported(R, C, n_keep)) {
+    if (!h.dry) CTM_CUDA(cudaEventRecord(h.ev[2], h.stream));
+    const double ms0 = h.ms_svd;
+    bool ok = false;
+    const double gap = iso_left_vectors(h, mat, R, C, n_keep, out, signfix_launch, &ok);
+    if (!h.dry && ok) {   // iso_left_vectors synchronised the stream
+      CTM_CUDA(cudaEventRecord(h.ev[3], h.stream));
+      CTM_CUDA(cudaEventSynchronize(h.ev[3]));
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[2], h.ev[3]));
+      h.ms_svd = ms0 + ms;
+      if (gap < h.min_gap) h.min_gap = gap;
+      return gap;
+    }
+    if (!h.dry) ++h.n_svd_fallback;   // not certified: the dense cuSOLVER factorisation below
+    // (sizing pass: fall through so the workspace also covers the fallback)
+  }
   const Plan p = make_plan(R, C, n_keep);
   const int mn = std::min(p.m, p.n);
   const size_t mark = h.ws.top;

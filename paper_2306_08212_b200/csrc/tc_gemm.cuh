@@ -70,8 +70,8 @@ __device__ __forceinline__ int mode_offset(int idx, int nmodes, const int* ext, 
   return off;
 }
 
-__device__ __forceinline__ void cp_async8(unsigned smem_addr, const void* gmem, int bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_addr), "l"(gmem), "r"(bytes));
+__device__ __forceinline__ void cp_async8(unsigned smem_addr, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_addr), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
 
   // ---- per-thread load assignment (fixed across stages) -----------------------------
   // A: k-fast -> fixed kl, rows ml0 + j*(THREADS/BK);  m-fast -> fixed ml, kl0 + j*(THREADS/BM)
+  // Rows / columns past the matrix edge read row / column 0 (their results are never
+  // stored); only the K tail must be zero, and it is written with st.shared in the last
+  // (partial) k-tile, so full k-tiles issue plain cp.async with no predicates.
   constexpr bool akf = AKF, bkf = BKF;
   const int a_fix = akf ? (tid % BK) : (tid % BM);
   const int a_var0 = akf ? (tid / BK) : (tid / BM);
@@ -179,36 +182,49 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   int a_row[C_::A_PER];   // k-fast: offsets of my rows; m-fast: only a_row[0] used
   int b_col[C_::B_PER];
 #pragma unroll
-  for (int j = 0; j < C_::A_PER; ++j) a_row[j] = akf ? a_moff[a_var0 + j * a_step] : a_moff[a_fix];
+  for (int j = 0; j < C_::A_PER; ++j) a_row[j] = max(0, akf ? a_moff[a_var0 + j * a_step] : a_moff[a_fix]);
 #pragma unroll
-  for (int j = 0; j < C_::B_PER; ++j) b_col[j] = bkf ? b_noff[b_var0 + j * b_step] : b_noff[b_fix];
+  for (int j = 0; j < C_::B_PER; ++j) b_col[j] = max(0, bkf ? b_noff[b_var0 + j * b_step] : b_noff[b_fix]);
   const unsigned pipe_s = static_cast<unsigned>(__cvta_generic_to_shared(pipe));
 
-  auto load_stage = [&](int stage, int kt) {
+  // one quarter of a stage's loads (part = 0..3), so they interleave with the DMMA steps
+  constexpr int A_Q = (C_::A_PER + 3) / 4, B_Q = (C_::B_PER + 3) / 4;
+  auto load_part = [&](int stage, int kt, int part, bool full) {
     const unsigned As = pipe_s + stage * C_::STAGE_DOUBLES * 8;
     const unsigned Bs = As + BK * C_::LDA * 8;
     const int k0 = kt * BK;   // relative to kbase
 #pragma unroll
-    for (int j = 0; j < C_::A_PER; ++j) {
-      const int kl = akf ? a_fix : (a_var0 + j * a_step);
-      const int ml = akf ? (a_var0 + j * a_step) : a_fix;
-      const int k = k0 + kl;
-      const int ro = a_row[akf ? j : 0];
-      const bool ok = (k < kcount) & (ro >= 0);
-      const double* src = Ag + (ok ? ro + a_koff[k] : 0);
-      cp_async8(As + (kl * C_::LDA + ml) * 8, src, ok ? 8 : 0);
+    for (int jj = 0; jj < A_Q; ++jj) {
+      const int j = part * A_Q + jj;
+      if (j < C_::A_PER) {
+        const int kl = akf ? a_fix : (a_var0 + j * a_step);
+        const int ml = akf ? (a_var0 + j * a_step) : a_fix;
+        const int k = k0 + kl;
+        const unsigned dst = As + (kl * C_::LDA + ml) * 8;
+        if (full || k < kcount) {
+          cp_async8(dst, Ag + (a_row[akf ? j : 0] + a_koff[k]));
+        } else {
+          asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0));
+        }
+      }
     }
 #pragma unroll
-    for (int j = 0; j < C_::B_PER; ++j) {
-      const int kl = bkf ? b_fix : (b_var0 + j * b_step);
-      const int nl = bkf ? (b_var0 + j * b_step) : b_fix;
-      const int k = k0 + kl;
-      const int co = b_col[bkf ? j : 0];
-      const bool ok = (k < kcount) & (co >= 0);
-      const double* src = Bg + (ok ? co + b_koff[k] : 0);
-      cp_async8(Bs + (kl * C_::LDB + nl) * 8, src, ok ? 8 : 0);
+    for (int jj = 0; jj < B_Q; ++jj) {
+      const int j = part * B_Q + jj;
+      if (j < C_::B_PER) {
+        const int kl = bkf ? b_fix : (b_var0 + j * b_step);
+        const int nl = bkf ? (b_var0 + j * b_step) : b_fix;
+        const int k = k0 + kl;
+        const unsigned dst = Bs + (kl * C_::LDB + nl) * 8;
+        if (full || k < kcount) {
+          cp_async8(dst, Bg + (b_col[bkf ? j : 0] + b_koff[k]));
+        } else {
+          asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0));
+        }
+      }
     }
   };
+  const int ktiles_full = kcount / BK;   // k-tiles [0, ktiles_full) need no tail handling
 
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp / WN, wn = warp % WN;
@@ -222,19 +238,21 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   // ---- prologue ---------------------------------------------------------------------
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < ktiles) load_stage(s, s);
+    if (s < ktiles) {
+#pragma unroll
+      for (int part = 0; part < 4; ++part) load_part(s, s, part, s < ktiles_full);
+    }
     cp_async_commit();
   }
 
   // ---- main loop --------------------------------------------------------------------
+  static_assert(BK == 16, "the load interleave assumes 4 DMMA k-steps per k-tile");
   for (int kt = 0; kt < ktiles; ++kt) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    {
-      int nk = kt + STAGES - 1;
-      if (nk < ktiles) load_stage(nk % STAGES, nk);
-      cp_async_commit();
-    }
+    const int nk = kt + STAGES - 1;
+    const bool do_load = nk < ktiles;
+    const bool nfull = nk < ktiles_full;
     const double* As = pipe + (kt % STAGES) * C_::STAGE_DOUBLES;
     const double* Bs = As + BK * C_::LDA;
 #pragma unroll
@@ -244,11 +262,13 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
       for (int i = 0; i < C_::MT; ++i) af[i] = As[(kk + t) * C_::LDA + wm * C_::WTM + i * 8 + g];
 #pragma unroll
       for (int j = 0; j < C_::NT; ++j) bf[j] = Bs[(kk + t) * C_::LDB + wn * C_::WTN + j * 8 + g];
+      if (do_load) load_part(nk % STAGES, nk, kk / 4, nfull);
 #pragma unroll
       for (int i = 0; i < C_::MT; ++i)
 #pragma unroll
         for (int j = 0; j < C_::NT; ++j) dmma(acc[i][j], af[i], bf[j]);
     }
+    cp_async_commit();
   }
   cp_async_wait<0>();
 

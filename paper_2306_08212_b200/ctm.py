@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libctm.so")
 CTM_OK = 0
 CTM_W_CLAMPED = 100
 CTM_SEQUENTIAL = 0
-CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD = 0, 1, 2
+CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD, CTM_SVD_GRAM, CTM_SVD_ISO = 0, 1, 2, 3, 4
 CTM_FLAG_CHECK_FINITE = 1
 CTM_FLAG_MOVE_ONLY = 2
 CTM_FLAG_PROFILE = 4
@@ -48,7 +48,8 @@ class ctm_env(ctypes.Structure):
 class ctm_move_stats(ctypes.Structure):
     _fields_ = [("ms_total", c_double), ("ms_svd", c_double), ("ms_contract", c_double), ("flops", c_double),
                 ("min_gap", c_double), ("n_svd", c_int), ("n_kernels", c_int), ("ms_gemm", c_double),
-                ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double)]
+                ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double),
+                ("n_svd_fallback", c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -112,7 +113,7 @@ def _ptr(t):
 class CtmHandle:
     """Owns a ctm_handle and its torch-allocated workspace."""
 
-    def __init__(self, d, D, chi, chi_p=None, chi_pp=None, svd_algo=CTM_SVD_GESVDP, flags=0,
+    def __init__(self, d, D, chi, chi_p=None, chi_pp=None, svd_algo=CTM_SVD_ISO, flags=0,
                  svd_tol=0.0, stream=None, device="cuda"):
         import torch
         self.torch = torch
