@@ -57,7 +57,7 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
   CK(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big));
-  CK(cudaFuncSetAttribute(jacobi_lsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * LMAX * LMAX)));
+  CK(cudaFuncSetAttribute(jacobi_lsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * LMAX * (LMAX + 1))));
   auto timeit = [&](auto f, int reps) {
     f();
     CK(cudaDeviceSynchronize());
@@ -109,12 +109,12 @@ int main(int argc, char** argv) {
   std::vector<double> X((size_t)n * n);
   for (auto& v : X) v = urand(seed);
   CK(cudaMemcpy(dX, X.data(), 8ull * n * n, cudaMemcpyHostToDevice));
-  const size_t smem_j = (size_t)n * n * sizeof(double);
+  const size_t smem_j = (size_t)n * (n + 1) * sizeof(double);
   for (int sweeps : {1, 60}) {
     for (double tol : {1e-14, 1e-8}) {
       if (sweeps == 1 && tol > 1e-10) continue;
       CK(cudaMemset(dst, 0, 64));
-      double us = timeit([&]() { jacobi_lsv_kernel<<<1, 1024, smem_j>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, tol); }, 3);
+      double us = timeit([&]() { jacobi_lsv_kernel<<<1, jacobi_threads(n), smem_j>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, tol); }, 3);
       CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
       std::vector<double> U((size_t)n * n), sig(n);
       CK(cudaMemcpy(U.data(), dU, 8ull * n * n, cudaMemcpyDeviceToHost));
