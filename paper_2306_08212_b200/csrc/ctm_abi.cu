@@ -411,6 +411,80 @@ std::vector<int> corners(Handle& h, const std::vector<CornerJob>& jobs, bool top
   return r;
 }
 
+// ---------------------------------------------------------------------------------------
+// REDUCED strategy (Fig 3(a,b)): the exact reduced
+// environment M, the one-shot 4-leg isometry V = first chi left singular vectors of M as
+// (chi D^2) x chi ("chi D^2 x chi in FIG 3(b)"), and the absorption with V on both
+// cuts -- O(chi^3 D^4) where the sequential order is O(chi^3 D^3).  Same contraction order
+// as the oracle (oracle/ctm_oracle.py reduced_env_exact, absorb_one_shot, *_one_shot).
+// ---------------------------------------------------------------------------------------
+// M(q,kd,bd,q') = sum C1 T2 C2 T1 X X* T3 (the right half replaced by {C^2, T^3}); X is the
+// site in the picture orientation (s,u,l,d,r).  M is allocated first (it outlives the
+// intermediates, which reuse two buffers).
+Ten reduced_env_exact(Handle& h, const RenvIn& in, const double* Xraw, const double* Xbraw) {
+  const int d = h.prm.d, D = in.T1.ext[1];
+  const int cx = in.C1.ext[0], cz = in.T2.ext[3], cy = in.C2.ext[1], cq = in.T1.ext[0], cw = in.T3.ext[3];
+  Ten X{const_cast<double*>(Xraw), {d, D, D, D, D}};
+  Ten Xb{const_cast<double*>(Xbraw), {d, D, D, D, D}};
+  Ten M = alloc(h, {cq, D, D, cw});
+  const size_t mark = h.ws.top;
+  Ten R1 = alloc(h, {cx, D, D, cz});
+  Ten R2 = alloc(h, {cx, D, D, cy});
+  double* bufA = h.ws.take((size_t)D * D * cy * cq * D * D);       // R3 (kbyqlm), later R5 (yqdrew)
+  double* bufB = h.ws.take((size_t)D * cy * D * cq * d * D * D);   // R4 (bymqsdr)
+  Ten R3{bufA, {D, D, cy, cq, D, D}};
+  Ten R4{bufB, {D, cy, D, cq, d, D, D}};
+  Ten R5{bufA, {cy, cq, D, D, D, D}};
+  contract(h, op({&in.C1}, "xp"), op({&in.T2}, "pkbz"), out({&R1}, "xkbz"));     // C1 (d=x, r=p), T2 (l=p,ku,bu,r=z)
+  contract(h, op({&R1}, "xkbz"), op({&in.C2}, "zy"), out({&R2}, "xkby"));        // C2 (l=z, d=y)
+  contract(h, op({&R2}, "xkby"), op({&in.T1}, "qlmx"), out({&R3}, "kbyqlm"));    // T1 (d=q, kl, bl, u=x)
+  contract(h, op({&R3}, "kbyqlm"), op({&X}, "skldr"), out({&R4}, "bymqsdr"));    // X over ku, kl
+  contract(h, op({&R4}, "bymqsdr"), op({&Xb}, "sbmew"), out({&R5}, "yqdrew"));   // X* over s, bu, bl
+  contract(h, op({&R5}, "yqdrew"), op({&in.T3}, "yrwz"), out({&M}, "qdez"));     // T3 (u=y, kr, br, d=z)
+  h.ws.reset(mark);
+  return M;
+}
+
+// V(p,k,b,n): first n = min(chi, rows) left singular vectors of M as (p k b) x q'.
+Ten one_shot_isometry(Handle& h, const Ten& M, int chi) {
+  const int P = M.ext[0], K = M.ext[1], B = M.ext[2], F = M.ext[3];
+  const int n = std::min(chi, P * K * B);
+  Ten V = alloc(h, {P, K, B, n});
+  svd_left(h, M.p, P * K * B, F, n, V.p);
+  return V;
+}
+
+// T'(o1,kz,bz,o2) = sum V_in(p,ki,bi,o1) T(p,kf,bf,q) X(s,ki,kf,ko,kz) X*(s,bi,bf,bo,bz) V_out(q,ko,bo,o2)
+int absorb_one_shot(Handle& h, const Ten& T, const Site& X, const Ten& Vin, const Ten& Vout, Ten& res, double* ss) {
+  const int D = T.ext[1], d = X.bra.ext[0];
+  const int o1 = Vin.ext[3], q = T.ext[3];
+  const size_t mark = h.ws.top;
+  Ten Y1 = alloc(h, {D, D, o1, D, D, q});        // jkofgq
+  Ten Y2 = alloc(h, {D, o1, D, q, d, D, D});     // kogqsaz
+  Ten Y3{Y1.p, {o1, q, D, D, D, D}};             // oqazbw (reuses Y1: dead after Y2)
+  contract(h, op({&Vin}, "pjko"), op({&T}, "pfgq"), out({&Y1}, "jkofgq"));
+  contract(h, op({&Y1}, "jkofgq"), op({&X.ket}, "jfsaz"), out({&Y2}, "kogqsaz"));   // ket (in,face,s,out,far)
+  contract(h, op({&Y2}, "kogqsaz"), op({&X.bra}, "sgkbw"), out({&Y3}, "oqazbw"));   // bra (s,face,in,out,far)
+  std::vector<double*> sv;
+  if (ss) sv.push_back(ss);
+  int np = contract(h, op({&Y3}, "oqazbw"), op({&Vout}, "qabd"), out({&res}, "ozwd", sv));
+  h.ws.reset(mark);
+  return np;
+}
+
+// C^1'(o,r) = sum C1(x,p) T2(p,k,b,r) V(x,k,b,o);  C^4'(r,o) = sum C4(p,x) T4(r,k,b,p) V(x,k,b,o)
+int corner_one_shot(Handle& h, const Ten& C, const Ten& T, const Ten& V, Ten& res, double* ss, bool top) {
+  const int D = T.ext[1];
+  const size_t mark = h.ws.top;
+  Ten Y = alloc(h, {top ? C.ext[0] : C.ext[1], D, D, top ? T.ext[3] : T.ext[0]});   // xkbr
+  contract(h, op({&C}, top ? "xp" : "px"), op({&T}, top ? "pkbr" : "rkbp"), out({&Y}, "xkbr"));
+  std::vector<double*> sv;
+  if (ss) sv.push_back(ss);
+  int np = contract(h, op({&Y}, "xkbr"), op({&V}, "xkbo"), out({&res}, top ? "or" : "ro", sv));
+  h.ws.reset(mark);
+  return np;
+}
+
 void check_env(const ctm_env* e, const ctm_params& p) {
   for (int x = 0; x < 2; ++x)
     for (int j = 0; j < 8; ++j) {
@@ -525,10 +599,125 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
   h.ws.reset(mark);
 }
 
+// Normalise (Frobenius, reading R13) and commit the six new tensors of an absorption.
+void commit_six(Handle& h, ctm_env* env, Ten nT[2], Ten nC1[2], Ten nC4[2], const double* ss,
+                const std::vector<int>& nparts, int absorption) {
+  const ctm_params& p = h.prm;
+  if (!h.dry) {
+    std::vector<const double*> src;
+    std::vector<double*> dst;
+    std::vector<size_t> n;
+    for (int y = 0; y < 2; ++y) {
+      src.push_back(nT[y].p);
+      dst.push_back(env->T[y][0]);
+      n.push_back(nT[y].size());
+    }
+    for (int y = 0; y < 2; ++y) {
+      src.push_back(nC1[y].p);
+      dst.push_back(env->C[y][0]);
+      n.push_back(nC1[y].size());
+    }
+    for (int x = 0; x < 2; ++x) {
+      src.push_back(nC4[x].p);
+      dst.push_back(env->C[x][3]);
+      n.push_back(nC4[x].size());
+    }
+    scale_commit(h, src, dst, n, ss, nparts);
+    if (p.flags & CTM_FLAG_CHECK_FINITE) {
+      int* cnt = reinterpret_cast<int*>(h.dev_scalars);
+      CTM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), h.stream));
+      for (size_t i = 0; i < dst.size(); ++i) nonfinite_count(h, dst[i], n[i], cnt);
+      int hc = 0;
+      CTM_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
+      CTM_CUDA(cudaStreamSynchronize(h.stream));
+      if (hc) throw Error(CTM_E_NONFINITE, "non-finite entries after column absorption " + std::to_string(absorption));
+    }
+  }
+  for (int y = 0; y < 2; ++y) {
+    env->ext[y][4][0] = nT[y].ext[0];
+    env->ext[y][4][1] = nT[y].ext[3];
+    env->ext[y][0][0] = nC1[y].ext[0];
+    env->ext[y][0][1] = nC1[y].ext[1];
+  }
+  for (int x = 0; x < 2; ++x) {
+    env->ext[x][3][0] = nC4[x].ext[0];
+    env->ext[x][3][1] = nC4[x].ext[1];
+  }
+}
+
+// REDUCED column absorption (P:L43 with P:L53's projectors): the two cut types' exact
+// reduced environments and one-shot isometries run concurrently on worker sub-handles 0/1.
+void column_absorption_reduced(Handle& h, const Site sl[2], const double* raw[2], ctm_env* env, int absorption) {
+  const ctm_params& p = h.prm;
+  const int D = p.D;
+  const size_t mark = h.ws.top;
+  Ten V[2][2];   // V[x][y]: cut 'xy' (x above)
+  for (auto& sub : h.subs) {
+    sub_begin(*sub);
+    sub->dry = h.dry;
+    sub->ws.reset(0);
+  }
+  if (!h.dry) {
+    CTM_CUDA(cudaEventRecord(h.ev[4], h.stream));
+    for (int i = 0; i < 2; ++i) CTM_CUDA(cudaStreamWaitEvent(h.subs[i]->stream, h.ev[4], 0));
+  }
+  std::vector<std::function<void()>> tasks;
+  for (int x = 0; x < 2; ++x)
+    tasks.push_back([&, x]() {
+      Handle& s = *h.subs[x];
+      RenvIn ri{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), nullptr};
+      Ten M = reduced_env_exact(s, ri, raw[x], raw[x]);
+      V[x][1 - x] = one_shot_isometry(s, M, p.chi);
+    });
+  run_parallel(h, tasks);
+  for (int i = 0; i < 2; ++i) {
+    Handle& s = *h.subs[i];
+    if (!h.dry) {
+      CTM_CUDA(cudaEventRecord(s.ev[1], s.stream));
+      CTM_CUDA(cudaStreamWaitEvent(h.stream, s.ev[1], 0));
+    }
+    sub_merge(h, s);
+  }
+  if (!h.dry) {
+    CTM_CUDA(cudaEventRecord(h.ev[5], h.stream));
+    CTM_CUDA(cudaEventSynchronize(h.ev[5]));
+    float ms = 0.f;
+    CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[4], h.ev[5]));
+    h.ms_iso += ms;
+  }
+  double* ss = h.ws.take(6 * (size_t)CTM_SS_SLOTS);
+  Ten nT[2], nC1[2], nC4[2];
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    nT[y] = alloc(h, {V[x][y].ext[3], D, D, V[y][x].ext[3]});
+    nC1[y] = alloc(h, {V[y][x].ext[3], envT(env, x, 2, D).ext[3]});
+    nC4[x] = alloc(h, {envT(env, y, 4, D).ext[0], V[y][x].ext[3]});
+  }
+  std::vector<int> np(6);
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    np[y] = absorb_one_shot(h, envT(env, x, 1, D), sl[x], V[x][y], V[y][x], nT[y], ss + (size_t)y * CTM_SS_SLOTS);
+    np[2 + y] = corner_one_shot(h, envC(env, x, 1), envT(env, x, 2, D), V[y][x], nC1[y],
+                                ss + (size_t)(2 + y) * CTM_SS_SLOTS, true);
+    np[4 + x] = corner_one_shot(h, envC(env, y, 4), envT(env, y, 4, D), V[y][x], nC4[x],
+                                ss + (size_t)(4 + x) * CTM_SS_SLOTS, false);
+  }
+  commit_six(h, env, nT, nC1, nC4, ss, np, absorption);
+  h.ws.reset(mark);
+}
+
 void left_move(Handle& h, const double* A, const double* B, ctm_env* env, const double* iso_in, double* iso_out) {
   const ctm_params& p = h.prm;
   const size_t mark = h.ws.top;
   Site sl[2] = {site_left(h, A, p.d, p.D), site_left(h, B, p.d, p.D)};
+  if (p.strategy == CTM_REDUCED_EXACT) {
+    if (iso_in || iso_out) throw Error(CTM_E_UNSUPPORTED, "iso_in / iso_out are defined for CTM_SEQUENTIAL only");
+    const double* raw[2] = {A, B};
+    column_absorption_reduced(h, sl, raw, env, 0);
+    column_absorption_reduced(h, sl, raw, env, 1);
+    h.ws.reset(mark);
+    return;
+  }
   Site st[2];
   if (!iso_in) {
     st[0] = site_top(h, A, p.d, p.D);
@@ -834,6 +1023,10 @@ void size_workspace(Handle& h) {
     ctm::RenvIn ri{{dummy, {c, c}}, {dummy, {c, D, D, c}}, {dummy, {c, c}}, {dummy, {c, D, D, c}},
                    {dummy, {c, D, D, c}}, &st};
     ctm::reduced_env(h, ri, p.chi_pp);
+    if (!(p.flags & CTM_FLAG_MOVE_ONLY) || p.strategy == CTM_REDUCED_EXACT) {   // ctm_reduced_env(EXACT)
+      h.ws.reset(0);
+      ctm::reduced_env_exact(h, ri, dummy, dummy);
+    }
   }
   main_need = std::max(main_need, h.ws.peak);
   if (!(p.flags & CTM_FLAG_MOVE_ONLY)) {
@@ -897,7 +1090,7 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
   if (!out || !p) return CTM_E_ARG;
   *out = nullptr;
   if (p->d < 1 || p->D < 1 || p->chi < 1 || p->chi_p < 1 || p->chi_pp < 1) return CTM_E_ARG;
-  if (p->strategy != CTM_SEQUENTIAL) return CTM_E_UNSUPPORTED;
+  if (p->strategy != CTM_SEQUENTIAL && p->strategy != CTM_REDUCED_EXACT) return CTM_E_UNSUPPORTED;
   std::unique_ptr<ctm_handle_s> hh(new ctm_handle_s());
   Handle& h = hh->h;
   h.prm = *p;
@@ -1020,10 +1213,19 @@ int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const dou
                     double* iso_out) {
   return guarded(hh, [&](Handle& h) {
     if (!C1 || !T2 || !C2 || !T1 || !X || !Xbra || !T3 || !M_out) throw Error(CTM_E_ARG, "null pointer");
-    if (mode != CTM_RENV_APPROX) throw Error(CTM_E_UNSUPPORTED, "CTM_RENV_EXACT is NEXT on the GPU (oracle only)");
+    if (mode != CTM_RENV_APPROX && mode != CTM_RENV_EXACT) throw Error(CTM_E_ARG, "unknown reduced-env mode");
     begin_call(h);
     const ctm_params& p = h.prm;
     const int D = p.D, c = p.chi;
+    if (mode == CTM_RENV_EXACT) {
+      ctm::RenvIn ri{{const_cast<double*>(C1), {c, c}},       {const_cast<double*>(T2), {c, D, D, c}},
+                     {const_cast<double*>(C2), {c, c}},       {const_cast<double*>(T1), {c, D, D, c}},
+                     {const_cast<double*>(T3), {c, D, D, c}}, nullptr};
+      ctm::Ten M = ctm::reduced_env_exact(h, ri, X, Xbra);
+      CTM_CUDA(cudaMemcpyAsync(M_out, M.p, M.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
+      CTM_CUDA(cudaStreamSynchronize(h.stream));
+      return;
+    }
     ctm::Site st = ctm::make_site(h, X, Xbra, p.d, D, 2, 1, 4, 3);
     ctm::RenvIn ri{{const_cast<double*>(C1), {c, c}},       {const_cast<double*>(T2), {c, D, D, c}},
                    {const_cast<double*>(C2), {c, c}},       {const_cast<double*>(T1), {c, D, D, c}},

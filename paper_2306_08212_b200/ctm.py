@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libctm.so")
 
 CTM_OK = 0
 CTM_W_CLAMPED = 100
-CTM_SEQUENTIAL = 0
+CTM_SEQUENTIAL, CTM_REDUCED_EXACT = 0, 1
 CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD, CTM_SVD_GRAM, CTM_SVD_ISO = 0, 1, 2, 3, 4
 CTM_FLAG_CHECK_FINITE = 1
 CTM_FLAG_MOVE_ONLY = 2
@@ -114,7 +114,7 @@ class CtmHandle:
     """Owns a ctm_handle and its torch-allocated workspace."""
 
     def __init__(self, d, D, chi, chi_p=None, chi_pp=None, svd_algo=CTM_SVD_ISO, flags=0,
-                 svd_tol=0.0, stream=None, device="cuda"):
+                 svd_tol=0.0, stream=None, device="cuda", strategy=None):
         import torch
         self.torch = torch
         if not torch.cuda.is_available():
@@ -122,7 +122,7 @@ class CtmHandle:
         self.device = torch.device(device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self.params = ctm_params(d, D, chi, chi if chi_p is None else chi_p, chi if chi_pp is None else chi_pp,
-                                 CTM_SEQUENTIAL, svd_algo, svd_tol, flags)
+                                 CTM_SEQUENTIAL if strategy is None else strategy, svd_algo, svd_tol, flags)
         h = c_void_p()
         ws = c_size_t()
         rc = lib().ctm_init(byref(h), byref(self.params), self.stream.cuda_stream, byref(ws))

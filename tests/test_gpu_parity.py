@@ -322,3 +322,57 @@ def test_bond_energy_D1_closed_form():
     for bond in (ctm.CTM_BOND_H, ctm.CTM_BOND_V):
         e = h.ctm_bond_energy(T_(g["A"]), T_(g["B"]), env, T_(hop), bond)
         assert abs(e - want) <= 1e-12
+
+
+# ----------------------------------------------------------------------------------------
+# REDUCED strategy (Fig 3(a,b)): exact reduced environment and the
+# one-shot 4-leg isometry on the GPU
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("d,D,chi", [(2, 2, 8), (2, 4, 32), (2, 3, 20), (2, 6, 64)])
+def test_reduced_env_exact(d, D, chi):
+    """M_exact (gauge-free: its legs are existing bonds) entrywise against the oracle."""
+    cfg = ci.custom(d, D, chi, seed_index=300 + chi, decaying=D >= 6)
+    g = ci.generate(cfg)
+    C, T, A = g["C"], g["T"], g["A"]
+    x = "b"
+    M_ref = O.reduced_env_exact(C[(x, 1)], T[(x, 2)], C[(x, 2)], T[(x, 1)], A, A, T[(x, 3)])
+    h = ctm.CtmHandle(d, D, chi)
+    M = torch.empty((chi, D, D, chi), dtype=torch.float64, device=DEV)
+    h.ctm_reduced_env(T_(C[(x, 1)]), T_(T[(x, 2)]), T_(C[(x, 2)]), T_(T[(x, 1)]), T_(A), T_(A), T_(T[(x, 3)]), M,
+                      mode=ctm.CTM_RENV_EXACT)
+    assert rel_err(M.cpu().numpy(), M_ref) <= 1e-11
+
+
+def test_reduced_move_without_truncation_matches_oracle():
+    """No truncation (chi0 = 1 -> 4 -> 16, every isometry square): the REDUCED move is exact."""
+    cfg = ci.custom(2, 2, 16, chi0=1, seed_index=22)
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(2, 2, 16, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=ctm.CTM_REDUCED_EXACT)
+    env = ctm.Env.from_host(g["C"], g["T"], 2, 16)
+    h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
+    got = env.to_host()
+    ref = O.left_move({"C": g["C"], "T": g["T"]}, g["A"], g["B"], 16, strategy="reduced")
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+
+        def col(e):
+            c = np.einsum("xR,yklx,zmny,Sz->RklmnS", e["C"][(x, 1)], e["T"][(x, 1)], e["T"][(y, 1)], e["C"][(y, 4)])
+            return c / np.linalg.norm(c)
+        assert np.allclose(col(got), col(ref), atol=1e-12)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2_dl", "c3_dl"])
+def test_reduced_move_gauge_invariant(name):
+    """One REDUCED left move: the 2x2 norm of the new environment (a gauge-invariant
+    closure, evaluated by the oracle on both) agrees with the oracle's REDUCED move."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg, ci.ENV_INIT.get(name))
+    A, B = g["A"], g["B"]
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=ctm.CTM_REDUCED_EXACT)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    st = h.ctm_left_move(T_(A), T_(B), env)
+    assert st["n_svd"] == 4
+    ref = O.left_move({"C": g["C"], "T": g["T"]}, A, B, cfg.chi, strategy="reduced")
+    n_gpu = O.norm_2x2(env.to_host(), A, B)
+    n_ref = O.norm_2x2(ref, A, B)
+    assert abs(n_gpu - n_ref) <= 1e-9 * abs(n_ref)

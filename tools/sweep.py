@@ -22,15 +22,16 @@ from paper_2306_08212_b200 import ctm  # noqa: E402
 PEAK = 37.14   # measured FP64 DMMA peak (profiles/r01_probe_fp64.txt)
 
 
-def run(name, steps, svd):
+def run(name, steps, svd, strategy="sequential"):
     cfg = ci.CONFIGS[name]
     g = ci.generate(cfg)
     dev = torch.device("cuda")
     stream = torch.cuda.Stream(dev)
     algo = {"iso": ctm.CTM_SVD_ISO, "gesvdp": ctm.CTM_SVD_GESVDP}[svd]
     with torch.cuda.stream(stream):
+        strat = {"sequential": ctm.CTM_SEQUENTIAL, "reduced": ctm.CTM_REDUCED_EXACT}[strategy]
         h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, svd_algo=algo, flags=ctm.CTM_FLAG_MOVE_ONLY,
-                          stream=stream, device=dev)
+                          stream=stream, device=dev, strategy=strat)
         A = torch.from_numpy(g["A"]).to(dev)
         B = torch.from_numpy(g["B"]).to(dev)
         env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi, device=dev)
@@ -41,7 +42,10 @@ def run(name, steps, svd):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            st = h.ctm_left_move(A, B, env, iso_in=iso if inject else None, iso_out=None if inject else iso)
+            if strategy == "reduced":
+                st = h.ctm_left_move(A, B, env)
+            else:
+                st = h.ctm_left_move(A, B, env, iso_in=iso if inject else None, iso_out=None if inject else iso)
             e1.record(stream)
             e1.synchronize()
             return e0.elapsed_time(e1), st
@@ -49,14 +53,17 @@ def run(name, steps, svd):
         for _ in range(2):
             step(False)
         full = [step(False) for _ in range(steps)]
-        for _ in range(2):
-            step(True)
-        con = [step(True) for _ in range(steps)]
-    F = ctm.ctm_move_flops(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp)
+        if strategy == "reduced":   # no injected-isometry path: report the full move only
+            con = full
+        else:
+            for _ in range(2):
+                step(True)
+            con = [step(True) for _ in range(steps)]
+    F = ctm.ctm_move_flops(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp) if strategy == "sequential" else None
     Fc = con[0][1]["flops"]
     ms_full = float(np.median([t for t, _ in full]))
     ms_con = float(np.median([t for t, _ in con]))
-    return {"config": name, "d": cfg.d, "D": cfg.D, "chi": cfg.chi, "svd": svd,
+    return {"config": name, "d": cfg.d, "D": cfg.D, "chi": cfg.chi, "svd": svd, "strategy": strategy,
             "flops_per_move": F, "contraction_flops_per_move": Fc,
             "full_move_ms": ms_full, "full_moves_per_s": 1e3 / ms_full,
             "isometry_ms": float(np.median([s["ms_isometry"] for _, s in full])),
@@ -72,10 +79,12 @@ def main():
     ap.add_argument("--configs", default="c2,c3,c4,c5,c5_256")
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--svd", default="iso")
+    ap.add_argument("--strategies", default="sequential")
     a = ap.parse_args()
-    for name in a.configs.split(","):
-        torch.cuda.reset_peak_memory_stats()
-        print(json.dumps(run(name, a.steps, a.svd)), flush=True)
+    for strategy in a.strategies.split(","):
+        for name in a.configs.split(","):
+            torch.cuda.reset_peak_memory_stats()
+            print(json.dumps(run(name, a.steps, a.svd, strategy)), flush=True)
 
 
 if __name__ == "__main__":
