@@ -106,6 +106,24 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
+def max_over_ranks(vals, device=None):
+    """Element-wise max of per-rank timings over all ranks (torch.distributed; the bench uses
+    NCCL on GPUs, the CPU tests gloo).  Single process: returned unchanged."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [float(v) for v in vals]
+    t = torch.tensor([float(v) for v in vals], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return [float(x) for x in t.cpu()]
+
+
+def job_value(world, ms_per_step_max):
+    """Whole-job moves/s: every rank runs one independent replica move per step (replicas
+    only), timed by the slowest rank."""
+    return world * 1e3 / ms_per_step_max
+
+
 def run_oracle_sample(cfg, what="left_move"):
     """One left move of the oracle (bounded CPU sample); returns seconds."""
     from oracle import ctm_oracle as O
@@ -231,11 +249,7 @@ def bench_ours(args, cfg):
     t_step = float(np.mean(ms))
     t_c = float(np.mean(ms_c))
     t_e2e = float(np.mean(ms_e2e))
-    if world > 1:
-        import torch.distributed as dist
-        tt = torch.tensor([t_step, t_c, t_e2e], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_step, t_c, t_e2e = [float(x) for x in tt.cpu()]
+    t_step, t_c, t_e2e = max_over_ranks([t_step, t_c, t_e2e], device=dev)
     ms_svd = float(np.mean([s["ms_svd"] for s in stats]))
     ms_iso = float(np.mean([s["ms_isometry"] for s in stats]))
     gem_ms = float(np.mean([s["ms_gemm"] for s in pst]))
@@ -244,7 +258,7 @@ def bench_ours(args, cfg):
     achieved = gem_fl / (gem_ms * 1e-3) / 1e12
     if rank != 0:
         return
-    value = world * 1e3 / t_step
+    value = job_value(world, t_step)
     line = {
         "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
@@ -256,7 +270,7 @@ def bench_ours(args, cfg):
         "ms_isometry_stage_per_move": ms_iso, "ms_svd_calls_summed_per_move": ms_svd,
         "svd_fallbacks_per_move": float(np.mean([s.get("n_svd_fallback", 0) for s in stats])),
         "ms_absorb_per_move": t_step - ms_iso,
-        "contraction_only": {"moves_per_s": world * 1e3 / t_c, "ms_per_move": t_c,
+        "contraction_only": {"moves_per_s": job_value(world, t_c), "ms_per_move": t_c,
                              "flops_per_move": gem_fl, "tflops": gem_fl / (t_c * 1e-3) / 1e12,
                              "frac_of_fp64_peak": gem_fl / (t_c * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                              "note": "isometries injected (INJECT_ISO): chains + corners + commit only, "
@@ -268,7 +282,7 @@ def bench_ours(args, cfg):
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                      "traffic": None, "launches_per_step": gem_n, "ms_per_step": gem_ms,
                      "peak_source": "measured DMMA loop (profiles/r01_probe_fp64.txt); MEASURED_PEAKS.json has no FP64"},
-        "e2e": {"value": world * 1e3 / t_e2e, "unit": "moves/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": job_value(world, t_e2e), "unit": "moves/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
