@@ -60,7 +60,10 @@ extern "C" {
 
 /* strategies (ctm_params.strategy) */
 #define CTM_SEQUENTIAL 0     /* reduced env + sequential ket/bra order: the hot path  */
-#define CTM_REDUCED_EXACT 1  /* NEXT on the GPU (oracle only in round 1)               */
+#define CTM_REDUCED_EXACT 1  /* exact reduced env M (Fig 3(b)) + one-shot 4-leg
+                                isometry from M as (chi D^2) x chi; O(chi^3 D^4)           */
+#define CTM_STANDARD 2       /* 8-tensor upper half of Fig 1(d) (Fig 2(c)) + one-shot
+                                isometry from (chi D^2) x (D^2 chi); O(chi^3 D^6)          */
 
 /* SVD back-ends (ctm_params.svd_algo); all on the device, no CPU fallback */
 #define CTM_SVD_GESVDP 0     /* cuSOLVER Xgesvdp (polar decomposition)                */

@@ -445,9 +445,47 @@ Ten reduced_env_exact(Handle& h, const RenvIn& in, const double* Xraw, const dou
   return M;
 }
 
-// V(p,k,b,n): first n = min(chi, rows) left singular vectors of M as (p k b) x q'.
+// STANDARD ("8 individual tensors", Fig 2(c)): upper half of the 2x2 patch
+//        C_x^1  T_x^2  T_y^2  C_y^2
+//        T_x^1    X      Y    T_y^3
+// open at the bottom: M_std(q, kX, bX, kY, bY, q').  Oracle order (half_network_standard).
+Ten half_network_standard(Handle& h, const Ten& C1x, const Ten& T2x, const Ten& T2y, const Ten& C2y, const Ten& T1x,
+                          const double* Xr, const double* Yr, const Ten& T3y) {
+  const int d = h.prm.d, D = T1x.ext[1];
+  Ten X{const_cast<double*>(Xr), {d, D, D, D, D}};
+  Ten Y{const_cast<double*>(Yr), {d, D, D, D, D}};
+  const int cP = T1x.ext[0], cf = C1x.ext[1], ci = T2x.ext[3], cl = T2y.ext[3], cm = C2y.ext[1], cQ = T3y.ext[3];
+  Ten M = alloc(h, {cP, D, D, D, D, cQ});
+  const size_t mark = h.ws.top;
+  // left half: C1x(d=e, r=f) T1x(d=P, kl=p, bl=q, u=e) T2x(l=f, ku=g, bu=h, r=i) X(s,u=g,l=p,d=K,r=r) X*(s,u=h,l=q,d=B,r=w)
+  Ten L1 = alloc(h, {cf, cP, D, D});
+  Ten L2 = alloc(h, {cP, D, D, D, D, ci});
+  Ten L3 = alloc(h, {cP, D, D, ci, d, D, D});
+  Ten L4 = alloc(h, {cP, ci, D, D, D, D});
+  contract(h, op({&C1x}, "ef"), op({&T1x}, "Ppqe"), out({&L1}, "fPpq"));
+  contract(h, op({&L1}, "fPpq"), op({&T2x}, "fghi"), out({&L2}, "Ppqghi"));
+  contract(h, op({&L2}, "Ppqghi"), op({&X}, "sgpKr"), out({&L3}, "PqhisKr"));
+  contract(h, op({&L3}, "PqhisKr"), op({&X}, "shqBw"), out({&L4}, "PiKrBw"));
+  // right half: T2y(l=i, ku=j, bu=k, r=l) C2y(l=l, d=m) T3y(u=m, kr=n, br=o, d=Q) Y(s,u=j,l=r,d=L,r=n) Y*(s,u=k,l=w,d=E,r=o)
+  Ten R1 = alloc(h, {ci, D, D, cm});
+  Ten R2 = alloc(h, {ci, D, D, D, D, cQ});
+  Ten R3 = alloc(h, {ci, D, D, cQ, d, D, D});
+  Ten R4 = alloc(h, {ci, cQ, D, D, D, D});
+  contract(h, op({&T2y}, "ijkl"), op({&C2y}, "lm"), out({&R1}, "ijkm"));
+  contract(h, op({&R1}, "ijkm"), op({&T3y}, "mnoQ"), out({&R2}, "ijknoQ"));
+  contract(h, op({&R2}, "ijknoQ"), op({&Y}, "sjrLn"), out({&R3}, "ikoQsrL"));
+  contract(h, op({&R3}, "ikoQsrL"), op({&Y}, "skwEo"), out({&R4}, "iQrLwE"));
+  contract(h, op({&L4}, "PiKrBw"), op({&R4}, "iQrLwE"), out({&M}, "PKBLEQ"));
+  (void)cl;
+  h.ws.reset(mark);
+  return M;
+}
+
+// V(p,k,b,n): first n = min(chi, rows) left singular vectors of M as (p k b) x (rest).
 Ten one_shot_isometry(Handle& h, const Ten& M, int chi) {
-  const int P = M.ext[0], K = M.ext[1], B = M.ext[2], F = M.ext[3];
+  const int P = M.ext[0], K = M.ext[1], B = M.ext[2];
+  int F = 1;
+  for (size_t i = 3; i < M.ext.size(); ++i) F *= M.ext[i];
   const int n = std::min(chi, P * K * B);
   Ten V = alloc(h, {P, K, B, n});
   svd_left(h, M.p, P * K * B, F, n, V.p);
@@ -665,9 +703,16 @@ void column_absorption_reduced(Handle& h, const Site sl[2], const double* raw[2]
   for (int x = 0; x < 2; ++x)
     tasks.push_back([&, x]() {
       Handle& s = *h.subs[x];
-      RenvIn ri{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), nullptr};
-      Ten M = reduced_env_exact(s, ri, raw[x], raw[x]);
-      V[x][1 - x] = one_shot_isometry(s, M, p.chi);
+      const int y = 1 - x;
+      Ten M;
+      if (p.strategy == CTM_STANDARD) {
+        M = half_network_standard(s, envC(env, x, 1), envT(env, x, 2, D), envT(env, y, 2, D), envC(env, y, 2),
+                                  envT(env, x, 1, D), raw[x], raw[y], envT(env, y, 3, D));
+      } else {
+        RenvIn ri{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), nullptr};
+        M = reduced_env_exact(s, ri, raw[x], raw[x]);
+      }
+      V[x][y] = one_shot_isometry(s, M, p.chi);
     });
   run_parallel(h, tasks);
   for (int i = 0; i < 2; ++i) {
@@ -710,7 +755,7 @@ void left_move(Handle& h, const double* A, const double* B, ctm_env* env, const 
   const ctm_params& p = h.prm;
   const size_t mark = h.ws.top;
   Site sl[2] = {site_left(h, A, p.d, p.D), site_left(h, B, p.d, p.D)};
-  if (p.strategy == CTM_REDUCED_EXACT) {
+  if (p.strategy == CTM_REDUCED_EXACT || p.strategy == CTM_STANDARD) {
     if (iso_in || iso_out) throw Error(CTM_E_UNSUPPORTED, "iso_in / iso_out are defined for CTM_SEQUENTIAL only");
     const double* raw[2] = {A, B};
     column_absorption_reduced(h, sl, raw, env, 0);
@@ -1090,7 +1135,8 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
   if (!out || !p) return CTM_E_ARG;
   *out = nullptr;
   if (p->d < 1 || p->D < 1 || p->chi < 1 || p->chi_p < 1 || p->chi_pp < 1) return CTM_E_ARG;
-  if (p->strategy != CTM_SEQUENTIAL && p->strategy != CTM_REDUCED_EXACT) return CTM_E_UNSUPPORTED;
+  if (p->strategy != CTM_SEQUENTIAL && p->strategy != CTM_REDUCED_EXACT && p->strategy != CTM_STANDARD)
+    return CTM_E_UNSUPPORTED;
   std::unique_ptr<ctm_handle_s> hh(new ctm_handle_s());
   Handle& h = hh->h;
   h.prm = *p;

@@ -18,7 +18,7 @@ LIB_PATH = os.path.join(HERE, "libctm.so")
 
 CTM_OK = 0
 CTM_W_CLAMPED = 100
-CTM_SEQUENTIAL, CTM_REDUCED_EXACT = 0, 1
+CTM_SEQUENTIAL, CTM_REDUCED_EXACT, CTM_STANDARD = 0, 1, 2
 CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD, CTM_SVD_GRAM, CTM_SVD_ISO = 0, 1, 2, 3, 4
 CTM_FLAG_CHECK_FINITE = 1
 CTM_FLAG_MOVE_ONLY = 2

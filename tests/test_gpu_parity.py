@@ -343,15 +343,20 @@ def test_reduced_env_exact(d, D, chi):
     assert rel_err(M.cpu().numpy(), M_ref) <= 1e-11
 
 
-def test_reduced_move_without_truncation_matches_oracle():
-    """No truncation (chi0 = 1 -> 4 -> 16, every isometry square): the REDUCED move is exact."""
+STRATS = {"reduced": "CTM_REDUCED_EXACT", "standard": "CTM_STANDARD"}
+
+
+@pytest.mark.parametrize("strategy", ["reduced", "standard"])
+def test_reduced_move_without_truncation_matches_oracle(strategy):
+    """No truncation (chi0 = 1 -> 4 -> 16, every isometry square): the REDUCED and STANDARD
+    moves are exact."""
     cfg = ci.custom(2, 2, 16, chi0=1, seed_index=22)
     g = ci.generate(cfg)
-    h = ctm.CtmHandle(2, 2, 16, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=ctm.CTM_REDUCED_EXACT)
+    h = ctm.CtmHandle(2, 2, 16, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=getattr(ctm, STRATS[strategy]))
     env = ctm.Env.from_host(g["C"], g["T"], 2, 16)
     h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
     got = env.to_host()
-    ref = O.left_move({"C": g["C"], "T": g["T"]}, g["A"], g["B"], 16, strategy="reduced")
+    ref = O.left_move({"C": g["C"], "T": g["T"]}, g["A"], g["B"], 16, strategy=strategy)
     for x in ("a", "b"):
         y = O.OTHER[x]
 
@@ -361,18 +366,20 @@ def test_reduced_move_without_truncation_matches_oracle():
         assert np.allclose(col(got), col(ref), atol=1e-12)
 
 
-@pytest.mark.parametrize("name", ["tiny", "c2_dl", "c3_dl"])
-def test_reduced_move_gauge_invariant(name):
-    """One REDUCED left move: the 2x2 norm of the new environment (a gauge-invariant
-    closure, evaluated by the oracle on both) agrees with the oracle's REDUCED move."""
+@pytest.mark.parametrize("strategy,name", [("reduced", "tiny"), ("reduced", "c2_dl"), ("reduced", "c3_dl"),
+                                           ("standard", "tiny"), ("standard", "c2_dl")])
+def test_reduced_move_gauge_invariant(strategy, name):
+    """One REDUCED / STANDARD left move: the 2x2 norm of the new environment (a
+    gauge-invariant closure, evaluated by the oracle on both) agrees with the oracle's move
+    of the same strategy."""
     cfg = ci.CONFIGS[name]
     g = ci.generate(cfg, ci.ENV_INIT.get(name))
     A, B = g["A"], g["B"]
-    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=ctm.CTM_REDUCED_EXACT)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=getattr(ctm, STRATS[strategy]))
     env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
     st = h.ctm_left_move(T_(A), T_(B), env)
     assert st["n_svd"] == 4
-    ref = O.left_move({"C": g["C"], "T": g["T"]}, A, B, cfg.chi, strategy="reduced")
+    ref = O.left_move({"C": g["C"], "T": g["T"]}, A, B, cfg.chi, strategy=strategy)
     n_gpu = O.norm_2x2(env.to_host(), A, B)
     n_ref = O.norm_2x2(ref, A, B)
     assert abs(n_gpu - n_ref) <= 1e-9 * abs(n_ref)

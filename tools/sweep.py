@@ -29,7 +29,8 @@ def run(name, steps, svd, strategy="sequential"):
     stream = torch.cuda.Stream(dev)
     algo = {"iso": ctm.CTM_SVD_ISO, "gesvdp": ctm.CTM_SVD_GESVDP}[svd]
     with torch.cuda.stream(stream):
-        strat = {"sequential": ctm.CTM_SEQUENTIAL, "reduced": ctm.CTM_REDUCED_EXACT}[strategy]
+        strat = {"sequential": ctm.CTM_SEQUENTIAL, "reduced": ctm.CTM_REDUCED_EXACT,
+                 "standard": ctm.CTM_STANDARD}[strategy]
         h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, svd_algo=algo, flags=ctm.CTM_FLAG_MOVE_ONLY,
                           stream=stream, device=dev, strategy=strat)
         A = torch.from_numpy(g["A"]).to(dev)
@@ -42,7 +43,7 @@ def run(name, steps, svd, strategy="sequential"):
             flush.zero_()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            if strategy == "reduced":
+            if strategy != "sequential":
                 st = h.ctm_left_move(A, B, env)
             else:
                 st = h.ctm_left_move(A, B, env, iso_in=iso if inject else None, iso_out=None if inject else iso)
@@ -53,7 +54,7 @@ def run(name, steps, svd, strategy="sequential"):
         for _ in range(2):
             step(False)
         full = [step(False) for _ in range(steps)]
-        if strategy == "reduced":   # no injected-isometry path: report the full move only
+        if strategy != "sequential":   # no injected-isometry path: report the full move only
             con = full
         else:
             for _ in range(2):
