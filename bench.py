@@ -106,6 +106,15 @@ def dist_setup(n_gpus):
     return world, rank, local
 
 
+def traffic_bytes(cfg):
+    """DRAM bytes per contraction-only step of tc_gemm, measured by ncu --set full for C4
+    (profiles/r01_final_traffic.json); None for other configs or when the file is absent."""
+    path = os.path.join(ROOT, "profiles", "r01_final_traffic.json")
+    if cfg.name != "c4" or not os.path.exists(path):
+        return None
+    return json.load(open(path))["dram_bytes_per_step"]
+
+
 def max_over_ranks(vals, device=None):
     """Element-wise max of per-rank timings over all ranks (torch.distributed; the bench uses
     NCCL on GPUs, the CPU tests gloo).  Single process: returned unchanged."""
@@ -134,6 +143,11 @@ def run_oracle_sample(cfg, what="left_move"):
     return time.perf_counter() - t
 
 
+def workload(cfg):
+    return (f"{cfg.name}: left move, d={cfg.d} D={cfg.D} chi={cfg.chi} chi'={cfg.chi_p} chi''={cfg.chi_pp}, "
+            f"sequential order")
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -154,8 +168,7 @@ def bench_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sec / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, ctm_inputs.py)",
-            "config": {"workload": f"{cfg.name}: left move, d={cfg.d} D={cfg.D} chi={cfg.chi} chi'={cfg.chi_p} "
-                                   f"chi''={cfg.chi_pp}, sequential order", "D": cfg.D, "chi": cfg.chi},
+            "config": {"workload": workload(cfg), "D": cfg.D, "chi": cfg.chi},
             "cpu_baseline": {"value": value, "unit": "moves/s", "cores": host_cores(), "kind": "oracle",
                              "sample": f"{args.steps} full left moves of {cfg.name} (NumPy/OpenBLAS fp64 oracle)"},
             "e2e": {"value": value, "unit": "moves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -263,9 +276,8 @@ def bench_ours(args, cfg):
         "metric": METRIC, "value": value, "unit": "moves/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": t_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, ctm_inputs.py)",
-        "config": {"workload": f"{cfg.name}: left move, d={cfg.d} D={cfg.D} chi={cfg.chi} chi'={cfg.chi_p} "
-                               f"chi''={cfg.chi_pp}, sequential order, svd={args.svd}",
-                   "D": cfg.D, "chi": cfg.chi, "parallelism": f"replicas{world}",
+        "config": {"workload": workload(cfg), "D": cfg.D, "chi": cfg.chi, "svd": args.svd,
+                   "parallelism": f"replicas{world}",
                    "l2": "256 MB L2 flush between timed steps; intermediates > L2"},
         "ms_isometry_stage_per_move": ms_iso, "ms_svd_calls_summed_per_move": ms_svd,
         "svd_fallbacks_per_move": float(np.mean([s.get("n_svd_fallback", 0) for s in stats])),
@@ -280,7 +292,8 @@ def bench_ours(args, cfg):
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
         "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4)", "achieved": achieved,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
-                     "traffic": None, "launches_per_step": gem_n, "ms_per_step": gem_ms,
+                     "traffic": traffic_bytes(cfg), "traffic_unit": "DRAM bytes per step (ncu, profiles/r01_final_traffic.json)",
+                     "launches_per_step": gem_n, "ms_per_step": gem_ms,
                      "peak_source": "measured DMMA loop (profiles/r01_probe_fp64.txt); MEASURED_PEAKS.json has no FP64"},
         "e2e": {"value": job_value(world, t_e2e), "unit": "moves/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
