@@ -304,7 +304,29 @@ void sub_merge(Handle& h, Handle& s) {
 // Isometry stage of one column absorption (rows a1-a5) on the worker sub-handles:
 // phase A: the four side TS (x in {a,b}) x (left, right) concurrently;
 // phase B: for each cut type the reduced env M_xy and the main TS(M; chi', chi).
-void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]) {
+// Right-side TS results of a left move.  A left move rewrites only C^1, T^1, C^4, so the
+// right-side products Q_r = C_x^2 T_x^3 -- and their isometries -- are identical in its two
+// column absorptions: the second absorption reuses the first one's (exact, not an
+// approximation).  Buffers live in the main arena for the duration of the move.
+struct SideCache {
+  bool valid = false;
+  SideOut side[2];   // x = a, b: right-side TS (v1, v2, Q2)
+};
+
+// Reserve the cache buffers in the caller's (left move's) part of the main arena.
+void reserve_side_cache(Handle& h, const ctm_env* env, SideCache& c) {
+  const ctm_params& p = h.prm;
+  const int D = p.D;
+  for (int x = 0; x < 2; ++x) {
+    const int P = envC(env, x, 2).ext[0], F = envT(env, x, 3, D).ext[3];
+    const int n1 = std::min(p.chi_pp, P * D), n2 = std::min(p.chi_pp, n1 * D);
+    c.side[x].v.v1 = alloc(h, {P, D, n1});
+    c.side[x].v.v2 = alloc(h, {n1, D, n2});
+    c.side[x].Q2 = alloc(h, {n1, D, F});
+  }
+}
+
+void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2], SideCache* cache = nullptr) {
   const ctm_params& p = h.prm;
   const int D = p.D;
   for (auto& s : h.subs) {
@@ -320,10 +342,31 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
   for (int x = 0; x < 2; ++x)
     ri[x] = RenvIn{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
   SideOut side[4];
+  const bool reuse = cache != nullptr && cache->valid;
   std::vector<std::function<void()>> A;
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 4; ++i) {
+    if (reuse && (i % 2) == 1) {
+      side[i] = cache->side[i / 2];
+      continue;
+    }
     A.push_back([&, i]() { side[i] = side_ts(*h.subs[i], ri[i / 2], (i % 2) == 0, p.chi_pp); });
+  }
   run_parallel(h, A);
+  if (cache != nullptr && !cache->valid) {
+    for (int x = 0; x < 2; ++x) {
+      Handle& sub = *h.subs[2 * x + 1];
+      const SideOut& o = side[2 * x + 1];
+      Ten* dst[3] = {&cache->side[x].v.v1, &cache->side[x].v.v2, &cache->side[x].Q2};
+      const Ten* src[3] = {&o.v.v1, &o.v.v2, &o.Q2};
+      for (int t = 0; t < 3; ++t) {
+        if (dst[t]->size() != src[t]->size()) throw Error(CTM_E_ARG, "side cache: shape mismatch");
+        dst[t]->ext = src[t]->ext;
+        if (!h.dry)
+          CTM_CUDA(cudaMemcpyAsync(dst[t]->p, src[t]->p, src[t]->size() * 8, cudaMemcpyDeviceToDevice, sub.stream));
+      }
+    }
+    cache->valid = true;
+  }
   if (!h.dry)
     for (int x = 0; x < 2; ++x) {   // phase B of x runs on sub 2x and needs sub 2x+1's outputs
       Handle& r = *h.subs[2 * x + 1];
@@ -538,7 +581,7 @@ void check_env(const ctm_env* e, const ctm_params& p) {
 //   C_y^1 <- N[C_x^1 T_x^2 V_yx] ; T_y^1 <- N[V_xy T_x^1 X X* V_yx] ; C_x^4 <- N[V_yx C_y^4 T_y^4]
 // ---------------------------------------------------------------------------------------
 void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* env, const double* iso_in,
-                       double* iso_out, int absorption) {
+                       double* iso_out, int absorption, SideCache* cache = nullptr) {
   const ctm_params& p = h.prm;
   const int D = p.D;
   const size_t mark = h.ws.top;
@@ -552,7 +595,7 @@ void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* e
       v.v2 = Ten{const_cast<double*>(base + n1), {p.chi_p, D, p.chi}};
     }
   } else {
-    isometry_stage(h, env, st, V);
+    isometry_stage(h, env, st, V, cache);
   }
   if (iso_out) {
     const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
@@ -768,8 +811,10 @@ void left_move(Handle& h, const double* A, const double* B, ctm_env* env, const 
     st[0] = site_top(h, A, p.d, p.D);
     st[1] = site_top(h, B, p.d, p.D);
   }
-  column_absorption(h, sl, st, env, iso_in, iso_out, 0);
-  column_absorption(h, sl, st, env, iso_in, iso_out, 1);
+  SideCache cache;   // right-side TS shared by the two absorptions (see SideCache)
+  if (!iso_in) reserve_side_cache(h, env, cache);
+  column_absorption(h, sl, st, env, iso_in, iso_out, 0, iso_in ? nullptr : &cache);
+  column_absorption(h, sl, st, env, iso_in, iso_out, 1, iso_in ? nullptr : &cache);
   h.ws.reset(mark);
 }
 
