@@ -275,7 +275,9 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     GY(Y, P);
     sv.cholqr(Z, C, l, 2, true, Rz);         // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR2)
     // the first Rayleigh-Ritz only estimates the spectrum for the filter: loose Jacobi
-    sv.jacobi(Rz, l, 1, l, W, S, checks == 1 ? 1e-8 : 1e-14);   // the first one feeds estimates only
+    // the first Rayleigh-Ritz only seeds the filter bounds: a capped, loose Jacobi suffices
+    if (checks == 1) sv.jacobi(Rz, l, 1, l, W, S, 1e-6, 3);
+    else sv.jacobi(Rz, l, 1, l, W, S, 1e-14);
     sv.gemm(Y, "ia", {R, l}, W, "ab", {l, l}, U, "ib", {R, l});
     sv.gemm(P, "ia", {R, l}, W, "ab", {l, l}, PW, "ib", {R, l});
     if (h.dry) {   // sizing pass: also reserve the G-form GEMMs' split-K slabs
@@ -340,7 +342,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     const int mb = std::max(1, std::min(12, (int)std::floor(std::log(1e6) / (std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12))));
     // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
     // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
-    CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
+    // (after the capped first check W is not orthogonal: keep filtering Y itself)
+    if (checks > 1) CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
     int done = 0;
     while (done < need) {
       const int m = std::min(mb, need - done);
