@@ -51,7 +51,7 @@ def _iso_from_flat(p, chi, D, chi_p):
 # rows a6-a8: absorb/truncate chain with identical isometries
 # ----------------------------------------------------------------------------------------
 @pytest.mark.parametrize("d,D,chi,chi_p", [(2, 2, 8, 8), (2, 4, 32, 32), (2, 3, 37, 29), (2, 6, 64, 64),
-                                           (2, 8, 128, 128)])
+                                           (2, 8, 128, 128), (2, 10, 200, 200), (2, 10, 256, 256)])
 def test_absorb_truncate_identical_isometries(d, D, chi, chi_p):
     rng = np.random.default_rng(1000 + chi)
     T = rng.standard_normal((chi, D, D, chi))
@@ -141,8 +141,7 @@ def test_reduced_env_untruncated_equals_exact():
 # ----------------------------------------------------------------------------------------
 # rows a1-a11: left move; GPU isometries injected into the oracle -> entrywise parity
 # ----------------------------------------------------------------------------------------
-@pytest.mark.parametrize("name", ["tiny", "c2", "c3", "c4"])
-@pytest.mark.parametrize("svd", SVDS)
+@pytest.mark.parametrize("name,svd", [(n, s) for n in ["tiny", "c2", "c3", "c4"] for s in SVDS] + [("c5", "iso")])
 def test_left_move_entrywise_with_gpu_isometries(name, svd):
     cfg = ci.CONFIGS[name]
     g = ci.generate(cfg)
