@@ -1,6 +1,7 @@
 // tc_gemm.cu -- contraction planner (labels -> strided GEMM modes) and launcher for the
 // FP64 DMMA kernel of tc_gemm.cuh.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <map>
 
@@ -252,7 +253,12 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
   int best = 0, best_splits = 1;
   double best_score = -1;
   const long long ktiles_all = (K + 15) / 16;
+  static const int forced = [] {   // CTM_TC_CFG=0|1|2 pins the tile config (experiments)
+    const char* e = std::getenv("CTM_TC_CFG");
+    return e ? std::atoi(e) : -1;
+  }();
   for (int i = 0; i < 3; ++i) {
+    if (forced >= 0 && i != forced) continue;
     const CfgInfo& c = kCfgs[i];
     long long tm = (M + c.BM - 1) / c.BM, tn = (N + c.BN - 1) / c.BN;
     long long tiles = tm * tn * batch;

@@ -110,6 +110,25 @@ int main(int argc, char** argv) {
   for (auto& v : X) v = urand(seed);
   CK(cudaMemcpy(dX, X.data(), 8ull * n * n, cudaMemcpyHostToDevice));
   const size_t smem_j = (size_t)n * (n + 1) * sizeof(double);
+  CK(cudaFuncSetAttribute(jacobi_lsv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jacobi2_smem_bytes()));
+  for (int sweeps : {1, 60}) {
+    CK(cudaMemset(dst, 0, 64));
+    double us = timeit([&]() { jacobi_lsv2_kernel<<<2, jacobi2_threads(), jacobi2_smem_bytes()>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14); }, 3);
+    CK(cudaGetLastError());
+    CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
+    std::vector<double> U((size_t)n * n), sig(n);
+    CK(cudaMemcpy(U.data(), dU, 8ull * n * n, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(sig.data(), dSig, 8ull * n, cudaMemcpyDeviceToHost));
+    double o = 0;
+    for (int a = 0; a < n; ++a)
+      for (int b = 0; b < n; ++b) {
+        double t = 0;
+        for (int i = 0; i < n; ++i) t += U[(size_t)i * n + a] * U[(size_t)i * n + b];
+        o = std::max(o, std::fabs(t - (a == b ? 1.0 : 0.0)));
+      }
+    printf("{\"kernel\":\"jacobi2_cluster\",\"n\":%d,\"max_sweeps\":%d,\"sweeps\":%d,\"us\":%.1f,\"us_per_sweep\":%.1f,\"orth_err\":%.3e,\"s0\":%.6f,\"slast\":%.3e}\n",
+           n, sweeps, st[2], us, us / std::max(1, st[2]), o, sig[0], sig[n - 1]);
+  }
   for (int sweeps : {1, 60}) {
     for (double tol : {1e-14, 1e-8}) {
       if (sweeps == 1 && tol > 1e-10) continue;
