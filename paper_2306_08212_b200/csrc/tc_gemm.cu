@@ -226,6 +226,19 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     a.a_k[i] = (int)mk.s1[i];
     a.b_k[i] = (int)mk.s2[i];
   }
+  // round-up reciprocals (Granlund-Montgomery, 31-bit dividends): sh = ceil(log2 e),
+  // mag = floor(2^32 (2^sh - e) / e) + 1, q = (umulhi(i, mag) + i) >> sh
+  auto magic = [](int e, unsigned& mag, int& sh) {
+    int s2 = 0;
+    while ((1LL << s2) < e) ++s2;
+    sh = s2;
+    mag = (unsigned)((((unsigned long long)1 << 32) * (((unsigned long long)1 << s2) - (unsigned long long)e)) /
+                     (unsigned long long)e + 1ULL);
+    if (e == 1) mag = 0;
+  };
+  for (int i = 0; i < a.nm; ++i) magic(a.m_ext[i], a.m_mag[i], a.m_sh[i]);
+  for (int i = 0; i < a.nn; ++i) magic(a.n_ext[i], a.n_mag[i], a.n_sh[i]);
+  for (int i = 0; i < a.nk; ++i) magic(a.k_ext[i], a.k_mag[i], a.k_sh[i]);
   a.a_kfast = a_kfast;
   a.b_kfast = b_kfast;
   (void)c_nfast;
@@ -323,6 +336,7 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     TcArgs c = a;
     const long long len = std::min(chunk, k_last - j0);
     c.k_ext[lk] = (int)len;
+    magic(c.k_ext[lk], c.k_mag[lk], c.k_sh[lk]);
     c.K = (int)(k_inner * len);
     c.beta = j0 == 0 ? 0.0 : 1.0;
     c.splits = 1;

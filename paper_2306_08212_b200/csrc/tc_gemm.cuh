@@ -48,6 +48,10 @@ struct TcArgs {
   int a_m[CTM_MAXMODES], a_k[CTM_MAXMODES];
   int b_k[CTM_MAXMODES], b_n[CTM_MAXMODES];
   int c_m[CTM_MAXMODES], c_n[CTM_MAXMODES];
+  // round-up reciprocal of every mode extent (q = (umulhi(i, mag) + i) >> sh for i < 2^31),
+  // so the per-CTA offset tables need no integer divisions
+  unsigned m_mag[CTM_MAXMODES], n_mag[CTM_MAXMODES], k_mag[CTM_MAXMODES];
+  int m_sh[CTM_MAXMODES], n_sh[CTM_MAXMODES], k_sh[CTM_MAXMODES];
   int a_kfast, b_kfast;
   int splits, ktiles_per_split;
   double alpha;
@@ -68,6 +72,25 @@ __device__ __forceinline__ int mode_offset(int idx, int nmodes, const int* ext, 
     }
   }
   return off;
+}
+
+// Offsets of one multi-index in two operands at once, divisions by magic multiply.
+__device__ __forceinline__ void mode_offset2(int idx, int nmodes, const int* ext, const unsigned* mag, const int* sh,
+                                             const int* s1, const int* s2, int& o1, int& o2) {
+  int a = 0, b = 0;
+  unsigned u = (unsigned)idx;
+#pragma unroll
+  for (int j = 0; j < CTM_MAXMODES; ++j) {
+    if (j < nmodes) {
+      const unsigned q = (__umulhi(u, mag[j]) + u) >> sh[j];
+      const int r = (int)(u - q * (unsigned)ext[j]);
+      a += r * s1[j];
+      b += r * s2[j];
+      u = q;
+    }
+  }
+  o1 = a;
+  o2 = b;
 }
 
 __device__ __forceinline__ void cp_async8(unsigned smem_addr, const void* gmem) {
@@ -150,21 +173,21 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
 
   // ---- offset tables -------------------------------------------------------------
   for (int i = tid; i < BM; i += THREADS) {
-    int m = m0 + i;
-    bool ok = m < M;
-    a_moff[i] = ok ? mode_offset(m, args.nm, args.m_ext, args.a_m) : -1;
-    c_moff[i] = ok ? mode_offset(m, args.nm, args.m_ext, args.c_m) : -1;
+    const int m = m0 + i;
+    int oa = -1, oc = -1;
+    if (m < M) mode_offset2(m, args.nm, args.m_ext, args.m_mag, args.m_sh, args.a_m, args.c_m, oa, oc);
+    a_moff[i] = oa;
+    c_moff[i] = oc;
   }
   for (int i = tid; i < BN; i += THREADS) {
-    int n = n0 + i;
-    bool ok = n < N;
-    b_noff[i] = ok ? mode_offset(n, args.nn, args.n_ext, args.b_n) : -1;
-    c_noff[i] = ok ? mode_offset(n, args.nn, args.n_ext, args.c_n) : -1;
+    const int n = n0 + i;
+    int ob = -1, oc = -1;
+    if (n < N) mode_offset2(n, args.nn, args.n_ext, args.n_mag, args.n_sh, args.b_n, args.c_n, ob, oc);
+    b_noff[i] = ob;
+    c_noff[i] = oc;
   }
-  for (int k = tid; k < kcount; k += THREADS) {
-    a_koff[k] = mode_offset(kbase + k, args.nk, args.k_ext, args.a_k);
-    b_koff[k] = mode_offset(kbase + k, args.nk, args.k_ext, args.b_k);
-  }
+  for (int k = tid; k < kcount; k += THREADS)
+    mode_offset2(kbase + k, args.nk, args.k_ext, args.k_mag, args.k_sh, args.a_k, args.b_k, a_koff[k], b_koff[k]);
   __syncthreads();
 
   // ---- per-thread load assignment (fixed across stages) -----------------------------
