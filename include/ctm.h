@@ -203,6 +203,16 @@ int ctm_left_move(ctm_handle h, const double* A, const double* B, ctm_env* env,
  * can be adjusted accordingly").  ctm_iterate runs n_iter x (left, right, up, down). */
 int ctm_move(ctm_handle h, int dir, const double* A, const double* B, ctm_env* env,
              ctm_move_stats* st);
+/* ctm_converge: CTM iterations (left, right, up, down) until the corner spectra move by
+ * less than tol between iterations, at most max_iter ("N_CTM ~ 10-30 times, the
+ * environment tensors will become sufficiently converged").  Criterion (DESIGN.md reading
+ * R22): the singular values of each of the 8 corners, sorted and normalised to unit sum;
+ * distance = max over corners of the 1-norm of the difference (zero-padded).  Reports the
+ * iterations run and the last distance (host pointers, nullable).  Synchronises the
+ * stream. */
+int ctm_converge(ctm_handle h, const double* A, const double* B, ctm_env* env, int max_iter, double tol,
+                 int* iters_out, double* delta_out, ctm_move_stats* st);
+
 int ctm_iterate(ctm_handle h, const double* A, const double* B, ctm_env* env, int n_iter,
                 ctm_move_stats* st);
 

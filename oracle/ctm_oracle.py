@@ -374,6 +374,50 @@ def ctm_iteration(env, A, B, chi, chi_p=None, chi_pp=None, strategy="sequential"
 
 
 # ----------------------------------------------------------------------------------
+# Convergence of the CTM iteration ("After applying moves in four directions
+# N_CTM ~ 10-30 times, the environment tensors will become sufficiently converged";
+# criterion: reading R22 -- sorted corner spectra normalised to unit 1-norm, distance =
+# max over the 8 corners of the 1-norm of the difference, zero-padded)
+# ----------------------------------------------------------------------------------
+
+def corner_spectrum(C):
+    """Singular values of a corner, descending, normalised to unit sum (reading R22)."""
+    s = np.linalg.svd(C, compute_uv=False)
+    return s / s.sum()
+
+
+def corner_spectra(env):
+    return {key: corner_spectrum(C) for key, C in env["C"].items()}
+
+
+def spectra_distance(sp1, sp2):
+    """max over corners of sum_i |s_i - s'_i| (the shorter spectrum zero-padded)."""
+    out = 0.0
+    for key in sp1:
+        a, b = sp1[key], sp2[key]
+        n = max(a.size, b.size)
+        a = np.pad(a, (0, n - a.size))
+        b = np.pad(b, (0, n - b.size))
+        out = max(out, float(np.abs(a - b).sum()))
+    return out
+
+
+def converge(env, A, B, chi, tol, max_iter, chi_p=None, chi_pp=None, strategy="sequential"):
+    """CTM iterations until the corner spectra move by less than tol between iterations
+    (reading R22), at most max_iter.  Returns (env, iterations, last distance)."""
+    prev = corner_spectra(env)
+    delta = np.inf
+    for it in range(1, max_iter + 1):
+        env = ctm_iteration(env, A, B, chi, chi_p, chi_pp, strategy)
+        cur = corner_spectra(env)
+        delta = spectra_distance(prev, cur)
+        if delta < tol:
+            return env, it, delta
+        prev = cur
+    return env, max_iter, delta
+
+
+# ----------------------------------------------------------------------------------
 # Closures (P:L24 Fig 1(c,d); observables implied by P:L92, P:L100)
 # ----------------------------------------------------------------------------------
 

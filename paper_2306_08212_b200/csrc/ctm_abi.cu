@@ -1387,6 +1387,64 @@ int ctm_iterate(ctm_handle hh, const double* A, const double* B, ctm_env* env, i
   });
 }
 
+namespace {
+// Corner spectra normalised to unit sum and their distance (reading R22).
+std::vector<std::vector<double>> corner_spectra(Handle& h, const ctm_env* env) {
+  std::vector<std::vector<double>> out;
+  for (int x = 0; x < 2; ++x)
+    for (int k = 0; k < 4; ++k) {
+      const int r = env->ext[x][k][0], c = env->ext[x][k][1];
+      std::vector<double> sv(std::min(r, c));
+      ctm::singular_values(h, env->C[x][k], r, c, sv.data());
+      double t = 0.0;
+      for (double v : sv) t += v;
+      for (double& v : sv) v = t > 0.0 ? v / t : 0.0;
+      out.push_back(std::move(sv));
+    }
+  return out;
+}
+double spectra_distance(const std::vector<std::vector<double>>& a, const std::vector<std::vector<double>>& b) {
+  double out = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) {
+    const size_t n = std::max(a[i].size(), b[i].size());
+    double d = 0.0;
+    for (size_t j = 0; j < n; ++j) d += std::fabs((j < a[i].size() ? a[i][j] : 0.0) - (j < b[i].size() ? b[i][j] : 0.0));
+    out = std::max(out, d);
+  }
+  return out;
+}
+}  // namespace
+
+int ctm_converge(ctm_handle hh, const double* A, const double* B, ctm_env* env, int max_iter, double tol,
+                 int* iters_out, double* delta_out, ctm_move_stats* st) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || max_iter < 1 || !(tol >= 0.0)) throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    CTM_CUDA(cudaEventRecord(h.ev[0], h.stream));
+    auto prev = corner_spectra(h, env);
+    double delta = std::numeric_limits<double>::infinity();
+    int it = 0;
+    while (it < max_iter) {
+      ++it;
+      for (int dir : {CTM_LEFT, CTM_RIGHT, CTM_UP, CTM_DOWN}) ctm::move_dir(h, dir, A, B, env);
+      auto cur = corner_spectra(h, env);
+      delta = spectra_distance(prev, cur);
+      if (delta < tol) break;
+      prev = std::move(cur);
+    }
+    if (iters_out) *iters_out = it;
+    if (delta_out) *delta_out = delta;
+    CTM_CUDA(cudaEventRecord(h.ev[1], h.stream));
+    if (st) {
+      CTM_CUDA(cudaEventSynchronize(h.ev[1]));
+      float ms = 0;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
+      fill_stats(h, st, ms);
+    }
+  });
+}
+
 int ctm_norm_2x2(ctm_handle hh, const double* A, const double* B, const ctm_env* env, double* out_host,
                  double* cancel_ratio_host) {
   return guarded(hh, [&](Handle& h) {

@@ -123,6 +123,7 @@ double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* 
 // iso.cu: libctm's own truncated SVD (subspace iteration + CholQR + one-sided Jacobi).
 #define CTM_ISO_LMAX 160
 void iso_init_kernels();
+void singular_values(Handle& h, const double* mat, int R, int C, double* host_out);
 bool iso_supported(int R, int C, int n_keep);
 // ok = false when convergence could not be certified (caller falls back to cuSOLVER).
 double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,

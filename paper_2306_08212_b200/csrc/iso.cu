@@ -392,6 +392,42 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   return gap;
 }
 
+// Singular values (descending) of a row-major R x C matrix into host memory: the one-sided
+// Jacobi kernels for square matrices up to LMAX, cuSOLVER Xgesvd (values only) otherwise.
+void singular_values(Handle& h, const double* mat, int R, int C, double* host_out) {
+  const size_t mark = h.ws.top;
+  const int mn = std::min(R, C);
+  double* S = h.ws.take((size_t)mn);
+  if (h.dry) {
+    h.ws.take((size_t)R * C + 64);
+    h.ws.reset(mark);
+    return;
+  }
+  if (R == C && R <= LMAX) {
+    Solver sv(h);
+    sv.jacobi(mat, R, 0, 0, nullptr, S, 1e-14);
+    sv.check_status("singular values");
+  } else {
+    double* A = h.ws.take((size_t)R * C);
+    // column-major copy of the R x C row-major matrix = its transpose read row-major
+    permute(h, mat, {R, C}, {1, 0}, A);
+    size_t dws = 0, hws = 0;
+    if (cusolverDnXgesvd_bufferSize(h.solver, h.solver_params, 'N', 'N', R, C, CUDA_R_64F, A, R, CUDA_R_64F, S,
+                                    CUDA_R_64F, nullptr, 1, CUDA_R_64F, nullptr, 1, CUDA_R_64F, &dws, &hws) !=
+        CUSOLVER_STATUS_SUCCESS)
+      throw Error(CTM_E_SOLVER, "gesvd buffer size");
+    double* work = h.ws.take(dws / sizeof(double) + 1);
+    if (h.host_buf.size() < hws + 16) h.host_buf.resize(hws + 16);
+    if (cusolverDnXgesvd(h.solver, h.solver_params, 'N', 'N', R, C, CUDA_R_64F, A, R, CUDA_R_64F, S, CUDA_R_64F,
+                         nullptr, 1, CUDA_R_64F, nullptr, 1, CUDA_R_64F, work, dws, h.host_buf.data(),
+                         h.host_buf.size(), h.dev_info) != CUSOLVER_STATUS_SUCCESS)
+      throw Error(CTM_E_SOLVER, "gesvd (singular values) failed");
+  }
+  CTM_CUDA(cudaMemcpyAsync(host_out, S, sizeof(double) * mn, cudaMemcpyDeviceToHost, h.stream));
+  CTM_CUDA(cudaStreamSynchronize(h.stream));
+  h.ws.reset(mark);
+}
+
 double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
                         void (*signfix)(Handle&, const double*, long long, long long, int, int, double*), bool* ok) {
   *ok = true;

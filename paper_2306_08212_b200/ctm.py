@@ -78,6 +78,8 @@ def lib():
             "ctm_left_move": (c_int, [P, P, P, POINTER(ctm_env), P, P, POINTER(ctm_move_stats)]),
             "ctm_move": (c_int, [P, c_int, P, P, POINTER(ctm_env), POINTER(ctm_move_stats)]),
             "ctm_iterate": (c_int, [P, P, P, POINTER(ctm_env), c_int, POINTER(ctm_move_stats)]),
+            "ctm_converge": (c_int, [P, P, P, POINTER(ctm_env), c_int, c_double, POINTER(c_int), POINTER(c_double),
+                                     POINTER(ctm_move_stats)]),
             "ctm_norm_2x2": (c_int, [P, P, P, POINTER(ctm_env), POINTER(c_double), POINTER(c_double)]),
             "ctm_bond_energy": (c_int, [P, P, P, POINTER(ctm_env), P, c_int, P, POINTER(c_double)]),
             "ctm_move_flops": (c_double, [c_int, c_int, c_int, c_int, c_int]),
@@ -94,7 +96,7 @@ def lib():
 def exported_symbols():
     return ["ctm_abi_version", "ctm_init", "ctm_set_workspace", "ctm_set_stream", "ctm_destroy",
             "ctm_last_error", "ctm_reduced_env", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
-            "ctm_iterate", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
+            "ctm_iterate", "ctm_converge", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
 
 
 def ctm_move_flops(d, D, chi, chi_p=None, chi_pp=None):
@@ -174,6 +176,15 @@ class CtmHandle:
         st = ctm_move_stats()
         self._check(lib().ctm_move(self.h, DIRS[direction], _ptr(A), _ptr(B), byref(env.c), byref(st)))
         return st.as_dict()
+
+    def ctm_converge(self, A, B, env, max_iter, tol):
+        """Returns (iterations, last corner-spectrum distance, stats dict)."""
+        st = ctm_move_stats()
+        it = c_int()
+        delta = c_double()
+        self._check(lib().ctm_converge(self.h, _ptr(A), _ptr(B), byref(env.c), max_iter, tol, byref(it), byref(delta),
+                                       byref(st)))
+        return it.value, delta.value, st.as_dict()
 
     def ctm_iterate(self, A, B, env, n_iter):
         st = ctm_move_stats()

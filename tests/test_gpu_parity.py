@@ -383,3 +383,22 @@ def test_reduced_move_gauge_invariant(strategy, name):
     n_gpu = O.norm_2x2(env.to_host(), A, B)
     n_ref = O.norm_2x2(ref, A, B)
     assert abs(n_gpu - n_ref) <= 1e-9 * abs(n_ref)
+
+
+# ----------------------------------------------------------------------------------------
+# convergence loop (reading R22): corner spectra on the GPU vs the oracle
+# ----------------------------------------------------------------------------------------
+@pytest.mark.parametrize("max_iter,tol,want_iters", [(3, 0.0, 3), (10, 0.06, 2)])
+def test_converge_matches_oracle(max_iter, tol, want_iters):
+    cfg = ci.CONFIGS["c2_dl"]
+    g = ci.generate(cfg)
+    A, B = g["A"], g["B"]
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    it, delta, _ = h.ctm_converge(T_(A), T_(B), env, max_iter, tol)
+    ref_env, it_ref, delta_ref = O.converge({"C": g["C"], "T": g["T"]}, A, B, cfg.chi, tol, max_iter)
+    assert it == it_ref == want_iters
+    assert abs(delta - delta_ref) <= 1e-8 * abs(delta_ref)
+    n_gpu = O.norm_2x2(env.to_host(), A, B)
+    n_ref = O.norm_2x2(ref_env, A, B)
+    assert abs(n_gpu - n_ref) <= 1e-9 * abs(n_ref)

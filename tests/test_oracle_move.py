@@ -150,3 +150,42 @@ def test_truncating_move_shapes_and_isometries():
     for k, v in new["T"].items():
         assert v.shape == (8, 2, 2, 8)
     assert all(np.isfinite(s["gap"]) or s["gap"] == np.inf for s in stats)
+
+
+# ----------------------------------------------------------------------------------------
+# convergence criterion (reading R22)
+# ----------------------------------------------------------------------------------------
+def test_corner_spectrum_closed_form():
+    """diag(3, 2, 1) rotated by orthogonal matrices: spectrum (3, 2, 1) / 6."""
+    rng = np.random.default_rng(5)
+    Q1, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    Q2, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    C = Q1 @ np.diag([3.0, 2.0, 1.0]) @ Q2.T
+    assert np.allclose(O.corner_spectrum(C), [0.5, 1 / 3, 1 / 6], atol=1e-14)
+
+
+def test_spectra_distance_is_a_padded_l1_max():
+    a = {("a", 1): np.array([0.6, 0.4]), ("b", 1): np.array([1.0])}
+    b = {("a", 1): np.array([0.5, 0.3, 0.2]), ("b", 1): np.array([1.0])}
+    assert O.spectra_distance(a, b) == pytest.approx(0.1 + 0.1 + 0.2)
+    assert O.spectra_distance(a, a) == 0.0
+    assert O.spectra_distance(a, b) == O.spectra_distance(b, a)
+
+
+def test_converge_scalar_environment_in_one_sweep():
+    """D = 1, chi = 1: every tensor is a scalar, every spectrum is (1) -- stationary from
+    the first iteration (distance exactly 0)."""
+    cfg = ci.custom(2, 1, 1, seed_index=41)
+    g = ci.generate(cfg)
+    _, it, delta = O.converge({"C": g["C"], "T": g["T"]}, g["A"], g["B"], 1, 1e-12, 10)
+    assert it == 1 and delta == 0.0
+
+
+def test_converge_iterations_monotone_in_tol():
+    cfg = ci.CONFIGS["c2_dl"]
+    g = ci.generate(cfg)
+    env = {"C": g["C"], "T": g["T"]}
+    _, it_loose, d_loose = O.converge(env, g["A"], g["B"], cfg.chi, 1e-4, 30)
+    _, it_tight, d_tight = O.converge(env, g["A"], g["B"], cfg.chi, 1e-8, 30)
+    assert it_loose <= it_tight
+    assert d_tight < 1e-8 or it_tight == 30
