@@ -229,6 +229,13 @@ int ctm_norm_2x2(ctm_handle h, const double* A, const double* B, const ctm_env* 
  * e = Tr(rho h) with h (d,d,d,d) = <s_i s_j| h |s_i' s_j'> on the device.
  * rho_out (nullable, device): (d,d,d,d) as (s_A, s_B, t_A, t_B).
  * e_out_host: the energy.  Synchronises the stream. */
+/* ctm_site_spins: single-site spin expectations for d = 2 (S = sigma/2), from the H-bond
+ * 2x1-window rho by partial trace ("staggered magnetization"; DESIGN.md
+ * reading R23).  out_host[4] = <S^x>_A, <S^z>_A, <S^x>_B, <S^z>_B (<S^y> = 0 for real
+ * tensors); the staggered magnetisation is m_s = (|<S>_A| + |<S>_B|) / 2.  Synchronises
+ * the stream.  d != 2: CTM_E_UNSUPPORTED. */
+int ctm_site_spins(ctm_handle h, const double* A, const double* B, const ctm_env* env, double* out_host);
+
 int ctm_bond_energy(ctm_handle h, const double* A, const double* B, const ctm_env* env,
                     const double* hop, int bond, double* rho_out, double* e_out_host);
 

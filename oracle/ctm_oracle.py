@@ -496,6 +496,29 @@ def bond_rho(env, A, B, bond="H"):
     return _c("YUsrtw,YUSrTw->sStT", L, R)
 
 
+def site_spins(env, A, B):
+    """Single-site spin expectations <S^x>, <S^z> (S = sigma/2, d = 2; <S^y> = 0 for the
+    real states here) of A and B from the 2x1-window rho of the H bond by partial trace
+    ("staggered magnetization"; reading R23).  Returns ((Sx_A, Sz_A),
+    (Sx_B, Sz_B))."""
+    rho = bond_rho(env, A, B, "H")                      # (sA, sB, tA, tB)
+    rA = np.einsum("sutu->st", rho)
+    rB = np.einsum("usut->st", rho)
+    sx = np.array([[0.0, 0.5], [0.5, 0.0]])
+    sz = np.array([[0.5, 0.0], [0.0, -0.5]])
+    out = []
+    for r in (rA, rB):
+        r = 0.5 * (r + r.T) / np.trace(r)
+        out.append((float(np.trace(r @ sx)), float(np.trace(r @ sz))))
+    return tuple(out)
+
+
+def staggered_magnetization(env, A, B):
+    """m_s = (|<S>_A| + |<S>_B|) / 2 (reading R23)."""
+    (xa, za), (xb, zb) = site_spins(env, A, B)
+    return 0.5 * (np.hypot(xa, za) + np.hypot(xb, zb))
+
+
 def rho_matrix(rho):
     """rho(sA,sB,tA,tB) -> (sA sB) x (tA tB) matrix, symmetrised (rho + rho^T)/2
      and divided by its trace."""

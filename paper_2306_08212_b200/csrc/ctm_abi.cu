@@ -951,9 +951,10 @@ double norm_2x2_impl(Handle& h, const double* A, const double* B, const ctm_env*
 //   C_a^1 T_a^2 T_b^2 C_b^2 / T_a^1 A B T_b^3 / C_a^4 T_a^4 T_b^4 C_b^3
 // rho(sA,sB,tA,tB) = L(Y,U,sA,r,tA,w) R(Y,U,sB,r,tB,w); ket then bra absorbed per half
 // (peak intermediate chi^2 d^2 D^4) so it also runs at C4 sizes.
-double bond_energy_impl(Handle& h, const double* A, const double* B, const ctm_env* env, const double* hop,
-                        double* rho_out) {
+// The 2x1 window's unnormalised rho(sA, sB, tA, tB) (H bond), allocated in the arena.
+Ten bond_rho_raw(Handle& h, const double* A, const double* B, const ctm_env* env) {
   const int D = h.prm.D, d = h.prm.d;
+  Ten rho = alloc(h, {d, d, d, d});
   const size_t mark = h.ws.top;
   Ten sA{const_cast<double*>(A), {d, D, D, D, D}}, sB{const_cast<double*>(B), {d, D, D, D, D}};
   const int a = 0, b = 1;
@@ -987,8 +988,16 @@ double bond_energy_impl(Handle& h, const double* A, const double* B, const ctm_e
   contract(h, op({&c3}, "WV"), op({&u4}, "VpqU"), out({&H1}, "WUpq"));
   Ten R = alloc(h, {u2.ext[0], u4.ext[3], d, D, d, D});
   contract(h, op({&G4}, "YWSrpTwq"), op({&H1}, "WUpq"), out({&R}, "YUSrTw"));
-  Ten rho = alloc(h, {d, d, d, d});
   contract(h, op({&L}, "YUsrtw"), op({&R}, "YUSrTw"), out({&rho}, "sStT"));
+  h.ws.reset(mark);
+  return rho;
+}
+
+double bond_energy_impl(Handle& h, const double* A, const double* B, const ctm_env* env, const double* hop,
+                        double* rho_out) {
+  const int d = h.prm.d;
+  const size_t mark = h.ws.top;
+  Ten rho = bond_rho_raw(h, A, B, env);
   double* e_dev = h.ws.take(1);
   rho_finish(h, rho.p, hop, d, rho_out, e_dev);
   double e = 0.0;
@@ -998,6 +1007,20 @@ double bond_energy_impl(Handle& h, const double* A, const double* B, const ctm_e
   }
   h.ws.reset(mark);
   return e;
+}
+
+// <S^x>, <S^z> of A and B from the H-bond rho by partial trace (reading R23), d = 2.
+void site_spins_impl(Handle& h, const double* A, const double* B, const ctm_env* env, double* out_host) {
+  if (h.prm.d != 2) throw Error(CTM_E_UNSUPPORTED, "site spins are defined for d = 2 (spin 1/2)");
+  const size_t mark = h.ws.top;
+  Ten rho = bond_rho_raw(h, A, B, env);
+  double* o = h.ws.take(4);
+  site_spins(h, rho.p, o);
+  if (!h.dry) {
+    CTM_CUDA(cudaMemcpyAsync(out_host, o, 4 * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+  }
+  h.ws.reset(mark);
 }
 
 }  // namespace
@@ -1457,6 +1480,15 @@ int ctm_norm_2x2(ctm_handle hh, const double* A, const double* B, const ctm_env*
       double va = ctm::norm_2x2_impl(h, A, B, env, true);
       *cancel_ratio_host = va != 0.0 ? v / va : 0.0;
     }
+  });
+}
+
+int ctm_site_spins(ctm_handle hh, const double* A, const double* B, const ctm_env* env, double* out_host) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || !out_host) throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    ctm::site_spins_impl(h, A, B, env, out_host);
   });
 }
 

@@ -111,7 +111,9 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
                   const std::vector<size_t>& ns, const double* ss, const std::vector<int>& nparts);
 void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count);
 void abs_copy(Handle& h, const double* src, double* dst, size_t n);
-void dot(Handle& h, const double* a, const double* b, size_t n, double* out);   // out = a.b (device)
+void dot(Handle& h, const double* a, const double* b, size_t n, double* out);
+// rho (2,2,2,2) of the H bond -> (<Sx>_A, <Sz>_A, <Sx>_B, <Sz>_B) into out (device, 4 doubles)
+void site_spins(Handle& h, const double* rho, double* out);   // out = a.b (device)
 // rho (d,d,d,d) -> symmetrised, trace-normalised; e = Tr(rho h) into e_dev; rho_out nullable
 void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* rho_out, double* e_dev);
 

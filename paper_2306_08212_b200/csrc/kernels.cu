@@ -140,6 +140,26 @@ __global__ void rho_finish_kernel(const double* __restrict__ rho, const double* 
   }
 }
 
+// rho(sA, sB, tA, tB), d = 2: partial traces -> rho_A, rho_B (symmetrised, unit trace),
+// out = (<Sx>_A, <Sz>_A, <Sx>_B, <Sz>_B) with S = sigma / 2.
+__global__ void site_spins_kernel(const double* __restrict__ rho, double* __restrict__ out) {
+  if (threadIdx.x != 0) return;
+  double rA[2][2] = {}, rB[2][2] = {};
+  for (int s = 0; s < 2; ++s)
+    for (int t = 0; t < 2; ++t)
+      for (int u = 0; u < 2; ++u) {
+        rA[s][t] += rho[((s * 2 + u) * 2 + t) * 2 + u];
+        rB[s][t] += rho[((u * 2 + s) * 2 + u) * 2 + t];
+      }
+  const double (*rs[2])[2] = {rA, rB};
+  for (int i = 0; i < 2; ++i) {
+    const double (*r)[2] = rs[i];
+    const double tr = r[0][0] + r[1][1];
+    out[2 * i] = 0.5 * (r[0][1] + r[1][0]) / tr;        // Tr(rho_sym sigma_x) / 2
+    out[2 * i + 1] = 0.5 * (r[0][0] - r[1][1]) / tr;    // Tr(rho sigma_z) / 2
+  }
+}
+
 int grid_for(long long n, int threads = 256) {
   long long b = (n + threads - 1) / threads;
   long long cap = kSMs * 8;
@@ -222,6 +242,13 @@ void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count) {
 void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* rho_out, double* e_dev) {
   if (h.dry) return;
   rho_finish_kernel<<<1, 32, 0, h.stream>>>(rho, hop, d * d, rho_out, e_dev);
+  CTM_CUDA(cudaGetLastError());
+  h.count_kernel();
+}
+
+void site_spins(Handle& h, const double* rho, double* out) {
+  if (h.dry) return;
+  site_spins_kernel<<<1, 32, 0, h.stream>>>(rho, out);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }

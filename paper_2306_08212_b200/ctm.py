@@ -81,6 +81,7 @@ def lib():
             "ctm_converge": (c_int, [P, P, P, POINTER(ctm_env), c_int, c_double, POINTER(c_int), POINTER(c_double),
                                      POINTER(ctm_move_stats)]),
             "ctm_norm_2x2": (c_int, [P, P, P, POINTER(ctm_env), POINTER(c_double), POINTER(c_double)]),
+            "ctm_site_spins": (c_int, [P, P, P, POINTER(ctm_env), POINTER(c_double)]),
             "ctm_bond_energy": (c_int, [P, P, P, POINTER(ctm_env), P, c_int, P, POINTER(c_double)]),
             "ctm_move_flops": (c_double, [c_int, c_int, c_int, c_int, c_int]),
             "ctm_kernel_count": (c_int64, [P]),
@@ -96,7 +97,7 @@ def lib():
 def exported_symbols():
     return ["ctm_abi_version", "ctm_init", "ctm_set_workspace", "ctm_set_stream", "ctm_destroy",
             "ctm_last_error", "ctm_reduced_env", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
-            "ctm_iterate", "ctm_converge", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
+            "ctm_iterate", "ctm_converge", "ctm_site_spins", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
 
 
 def ctm_move_flops(d, D, chi, chi_p=None, chi_pp=None):
@@ -185,6 +186,14 @@ class CtmHandle:
         self._check(lib().ctm_converge(self.h, _ptr(A), _ptr(B), byref(env.c), max_iter, tol, byref(it), byref(delta),
                                        byref(st)))
         return it.value, delta.value, st.as_dict()
+
+    def ctm_site_spins(self, A, B, env):
+        """((Sx_A, Sz_A), (Sx_B, Sz_B)) and m_s = (|<S>_A| + |<S>_B|) / 2."""
+        o = (c_double * 4)()
+        self._check(lib().ctm_site_spins(self.h, _ptr(A), _ptr(B), byref(env.c), o))
+        sa, sb = (o[0], o[1]), (o[2], o[3])
+        ms = 0.5 * ((sa[0] ** 2 + sa[1] ** 2) ** 0.5 + (sb[0] ** 2 + sb[1] ** 2) ** 0.5)
+        return (sa, sb), ms
 
     def ctm_iterate(self, A, B, env, n_iter):
         st = ctm_move_stats()

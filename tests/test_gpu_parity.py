@@ -402,3 +402,16 @@ def test_converge_matches_oracle(max_iter, tol, want_iters):
     n_gpu = O.norm_2x2(env.to_host(), A, B)
     n_ref = O.norm_2x2(ref_env, A, B)
     assert abs(n_gpu - n_ref) <= 1e-9 * abs(n_ref)
+
+
+@pytest.mark.parametrize("name", ["tiny", "c2"])
+def test_site_spins(name):
+    """ctm_site_spins (GPU closure) vs the oracle on the same environment."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    (sa, sb), ms = h.ctm_site_spins(T_(g["A"]), T_(g["B"]), env)
+    ref = O.site_spins({"C": g["C"], "T": g["T"]}, g["A"], g["B"])
+    assert np.allclose(np.array([sa, sb]), np.array(ref), atol=1e-10, rtol=1e-10)
+    assert ms == pytest.approx(O.staggered_magnetization({"C": g["C"], "T": g["T"]}, g["A"], g["B"]), rel=1e-10)

@@ -155,3 +155,51 @@ def test_rho_trace_is_window_norm():
     R = np.einsum("jWU,VjU->WV", R, T[("b", 4)])
     want = np.einsum("WV,WV->", R, C[("b", 3)])
     assert np.isclose(tr, want, rtol=1e-11)
+
+
+# ----------------------------------------------------------------------------------------
+# single-site spins and staggered magnetisation (reading R23)
+# ----------------------------------------------------------------------------------------
+def _spin(phi):
+    phi = phi / np.linalg.norm(phi)
+    sx = np.array([[0.0, 0.5], [0.5, 0.0]])
+    sz = np.array([[0.5, 0.0], [0.0, -0.5]])
+    return phi @ sx @ phi, phi @ sz @ phi
+
+
+def test_site_spins_product_state_closed_form():
+    """A = phi(s) a(u) b(l) c(d) e(r): for ANY environment <S>_A = phi^T S phi / |phi|^2."""
+    rng = np.random.default_rng(40)
+    D = 2
+    env, _, _ = _env(ci.custom(2, D, 4, seed_index=40))
+
+    def prod_site():
+        vs = [rng.standard_normal(D) for _ in range(4)]
+        phi = rng.standard_normal(2)
+        return np.einsum("s,u,l,d,r->suldr", phi, *vs), phi
+    A, pa = prod_site()
+    B, pb = prod_site()
+    (xa, za), (xb, zb) = O.site_spins(env, A, B)
+    assert np.allclose((xa, za), _spin(pa), atol=1e-12)
+    assert np.allclose((xb, zb), _spin(pb), atol=1e-12)
+    want = 0.5 * (np.hypot(*_spin(pa)) + np.hypot(*_spin(pb)))
+    assert np.isclose(O.staggered_magnetization(env, A, B), want, rtol=1e-12)
+
+
+def test_site_spins_neel_state():
+    """Neel product state (A up, B down along z): <S^z> = +1/2, -1/2, m_s = 1/2."""
+    env, _, _ = _env(ci.custom(2, 1, 3, seed_index=42))
+    A = np.array([1.0, 0.0]).reshape(2, 1, 1, 1, 1)
+    B = np.array([0.0, 1.0]).reshape(2, 1, 1, 1, 1)
+    (xa, za), (xb, zb) = O.site_spins(env, A, B)
+    assert np.allclose((xa, za, xb, zb), (0.0, 0.5, 0.0, -0.5), atol=1e-14)
+    assert np.isclose(O.staggered_magnetization(env, A, B), 0.5)
+
+
+def test_site_spins_bounded_for_a_positive_environment():
+    """With the partial-trace (positive) start the window rho is a density matrix, so
+    |<S>| <= 1/2 (a Gaussian environment is not positive and carries no such bound)."""
+    cfg = ci.custom(2, 2, 4, seed_index=43)
+    g = ci.generate(cfg, "double_layer")
+    for x, z in O.site_spins({"C": g["C"], "T": g["T"]}, g["A"], g["B"]):
+        assert np.hypot(x, z) <= 0.5 + 1e-12
