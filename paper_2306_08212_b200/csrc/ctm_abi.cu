@@ -6,6 +6,7 @@
 //
 // Citations: P:Lnn = PAPER.md line; rows a1..a11 and S1..S6 = SURVEY.md 8(a).
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -1136,28 +1137,38 @@ void size_workspace(Handle& h) {
     ctm::RenvIn ri{{dummy, {c, c}}, {dummy, {c, D, D, c}}, {dummy, {c, c}}, {dummy, {c, D, D, c}},
                    {dummy, {c, D, D, c}}, &st};
     ctm::reduced_env(h, ri, p.chi_pp);
-    if (!(p.flags & CTM_FLAG_MOVE_ONLY) || p.strategy == CTM_REDUCED_EXACT) {   // ctm_reduced_env(EXACT)
-      h.ws.reset(0);
-      ctm::reduced_env_exact(h, ri, dummy, dummy);
+    main_need = std::max(main_need, h.ws.peak);
+    // optional entry points are sized when they fit the kernel's 2^31-element operand
+    // limit; otherwise the handle still serves moves and those calls report CTM_E_ARG /
+    // CTM_E_NOMEM when made (C5 at chi = 256: the closures' enlarged corners)
+    auto optional = [&](auto&& f) {
+      const size_t keep = main_need;
+      try {
+        h.ws.reset(0);
+        h.ws.peak = 0;
+        f();
+        main_need = std::max(keep, h.ws.peak);
+      } catch (const Error&) {
+        main_need = keep;
+      }
+    };
+    if (!(p.flags & CTM_FLAG_MOVE_ONLY) || p.strategy == CTM_REDUCED_EXACT)   // ctm_reduced_env(EXACT)
+      optional([&]() { ctm::reduced_env_exact(h, ri, dummy, dummy); });
+    if (!(p.flags & CTM_FLAG_MOVE_ONLY)) {
+      optional([&]() { ctm::norm_2x2_impl(h, dummy, dummy, &env, true); });
+      optional([&]() {
+        const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D;
+        h.ws.take(2 * ns);
+        ctm::bond_energy_impl(h, dummy, dummy, &env, dummy, nullptr);
+      });
     }
-  }
-  main_need = std::max(main_need, h.ws.peak);
-  if (!(p.flags & CTM_FLAG_MOVE_ONLY)) {
-    h.ws.reset(0);
-    h.ws.peak = 0;
-    ctm::norm_2x2_impl(h, dummy, dummy, &env, true);
-    main_need = std::max(main_need, h.ws.peak);
-    h.ws.reset(0);
-    h.ws.peak = 0;
-    const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D;
-    h.ws.take(2 * ns);
-    ctm::bond_energy_impl(h, dummy, dummy, &env, dummy, nullptr);
-    main_need = std::max(main_need, h.ws.peak);
   }
   set_dry(h, false);
   const size_t margin = (size_t)32 * 1024 * 1024;   // cuSOLVER workspace size variations
   h.main_bytes = (main_need + margin + 4095) & ~size_t(4095);
   h.sub_bytes = (sub_need + margin + 4095) & ~size_t(4095);
+  if (std::getenv("CTM_DEBUG_WS"))
+    fprintf(stderr, "[ws] main %.3f GB, %zu subs x %.3f GB\n", h.main_bytes / 1e9, h.subs.size(), h.sub_bytes / 1e9);
 }
 
 void init_solver(Handle& h, const ctm_params* p) {

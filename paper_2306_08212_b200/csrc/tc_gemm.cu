@@ -254,13 +254,6 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
   a.splits = 1;
   a.ktiles_per_split = (int)((K + 15) / 16);
   a.part = nullptr;
-  if (h.dry) {
-    // sizing pass: reserve the largest split-K slab this contraction could use
-    const size_t mark = h.ws.top;
-    h.ws.take((size_t)batch * 8 * M * N);
-    h.ws.reset(mark);
-    return 0;
-  }
   // tile-config choice: maximise (wave efficiency) x (tile fill) x (per-tile efficiency),
   // then split K when one wave is not filled (deterministic split-K reduction).
   int best = 0, best_splits = 1;
@@ -292,6 +285,16 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
       best = i;
       best_splits = splits;
     }
+  }
+  if (h.dry) {
+    // sizing pass: reserve exactly the split-K slab the real launch will take (the tile /
+    // split choice above depends on shapes only); no slab when the launch is not split
+    if (best_splits > 1) {
+      const size_t mark = h.ws.top;
+      h.ws.take((size_t)batch * best_splits * M * N);
+      h.ws.reset(mark);
+    }
+    return 0;
   }
   const bool prof = (h.prm.flags & CTM_FLAG_PROFILE) != 0;
   auto prof_begin = [&]() {
