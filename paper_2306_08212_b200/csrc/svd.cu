@@ -63,7 +63,7 @@ __global__ void extract_signfix_kernel(const double* __restrict__ base, long lon
         bi = oi;
       }
     }
-    if (l == 0) si[0] = bi;
+    if (l == 0) si[0] = bi < R ? bi : 0;   // all-NaN column: no arg-max (non-finite, reported later)
   }
   __syncthreads();
   const double sgn = col[(long long)si[0] * rs] < 0.0 ? -1.0 : 1.0;

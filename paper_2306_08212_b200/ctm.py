@@ -26,6 +26,7 @@ CTM_FLAG_PROFILE = 4
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
 DIRS = {"left": 0, "right": 1, "up": 2, "down": 3}
+CTM_E_ARG, CTM_E_CUDA, CTM_E_SOLVER, CTM_E_NONFINITE, CTM_E_NOMEM, CTM_E_UNSUPPORTED = 1, 2, 3, 4, 5, 6
 STATUS = {0: "CTM_OK", 1: "CTM_E_ARG", 2: "CTM_E_CUDA", 3: "CTM_E_SOLVER", 4: "CTM_E_NONFINITE",
           5: "CTM_E_NOMEM", 6: "CTM_E_UNSUPPORTED"}
 

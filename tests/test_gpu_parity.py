@@ -415,3 +415,59 @@ def test_site_spins(name):
     ref = O.site_spins({"C": g["C"], "T": g["T"]}, g["A"], g["B"])
     assert np.allclose(np.array([sa, sb]), np.array(ref), atol=1e-10, rtol=1e-10)
     assert ms == pytest.approx(O.staggered_magnetization({"C": g["C"], "T": g["T"]}, g["A"], g["B"]), rel=1e-10)
+
+
+# ----------------------------------------------------------------------------------------
+# error conventions on the device path (status codes, no exception across the ABI)
+# ----------------------------------------------------------------------------------------
+def test_errors_are_status_codes():
+    cfg = ci.CONFIGS["tiny"]
+    g = ci.generate(cfg)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    L = ctm.lib()
+    # null site pointer -> CTM_E_ARG with a message
+    assert L.ctm_left_move(h.h, None, None, ctypes_byref(env), None, None, None) == ctm.CTM_E_ARG
+    assert b"null" in L.ctm_last_error(h.h)
+    # boundary extent above chi -> CTM_E_ARG
+    env.c.ext[0][4][0] = cfg.chi + 1
+    with pytest.raises(ctm.CtmError) as ei:
+        h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
+    assert ei.value.code == ctm.CTM_E_ARG
+    env.c.ext[0][4][0] = cfg.chi
+    # iso_in / iso_out with the REDUCED strategy -> CTM_E_UNSUPPORTED
+    hr = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY, strategy=ctm.CTM_REDUCED_EXACT)
+    iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
+    with pytest.raises(ctm.CtmError) as ei:
+        hr.ctm_left_move(T_(g["A"]), T_(g["B"]), env, iso_out=iso)
+    assert ei.value.code == ctm.CTM_E_UNSUPPORTED
+    # the handle is still usable after an error
+    h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
+
+
+@pytest.mark.parametrize("name,svd", [("tiny", "iso"), ("c2", "iso"), ("c2", "gesvdp")])
+def test_non_finite_input_is_reported(name, svd):
+    """CHECK_FINITE: a NaN in the environment surfaces as CTM_E_NONFINITE / CTM_E_SOLVER
+    (S:L75), never as an illegal access or silently corrupted tensors."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    C = dict(g["C"])
+    C[("a", 1)] = C[("a", 1)].copy()
+    C[("a", 1)][0, 0] = np.nan
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, flags=ctm.CTM_FLAG_MOVE_ONLY | ctm.CTM_FLAG_CHECK_FINITE,
+                      svd_algo=svd_algo(svd))
+    env = ctm.Env.from_host(C, g["T"], cfg.D, cfg.chi)
+    with pytest.raises(ctm.CtmError) as ei:
+        h.ctm_left_move(T_(g["A"]), T_(g["B"]), env)
+    assert ei.value.code in (ctm.CTM_E_NONFINITE, ctm.CTM_E_SOLVER)
+
+
+def test_chi_p_above_chi_D_is_clamped_with_a_warning():
+    """chi' > chi D is clamped to chi D, reported as CTM_W_CLAMPED."""
+    h = ctm.CtmHandle(2, 2, 4, chi_p=100, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    assert h.clamped
+
+
+def ctypes_byref(env):
+    import ctypes
+    return ctypes.byref(env.c)
