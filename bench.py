@@ -226,6 +226,22 @@ def bench_ours(args, cfg):
         for _ in range(2):
             step(inject=True)
         ms_c = [step(inject=True) for _ in range(args.steps)]
+        # the same contraction-only move replayed from a CUDA graph (SURVEY 8(d) protocol 3)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=stream):
+            h.ctm_left_move(A, B, env, iso_in=iso, stats=False)
+        graph.replay()
+        stream.synchronize()
+        ms_g = []
+        for _ in range(args.steps):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            graph.replay()
+            e1.record(stream)
+            e1.synchronize()
+            ms_g.append(e0.elapsed_time(e1))
+        del graph
         # per-launch profile of the dominant kernel (tc_gemm), same contraction-only step
         pst = []
         for _ in range(3):
@@ -262,7 +278,8 @@ def bench_ours(args, cfg):
     t_step = float(np.mean(ms))
     t_c = float(np.mean(ms_c))
     t_e2e = float(np.mean(ms_e2e))
-    t_step, t_c, t_e2e = max_over_ranks([t_step, t_c, t_e2e], device=dev)
+    t_g = float(np.mean(ms_g))
+    t_step, t_c, t_e2e, t_g = max_over_ranks([t_step, t_c, t_e2e, t_g], device=dev)
     ms_svd = float(np.mean([s["ms_svd"] for s in stats]))
     ms_iso = float(np.mean([s["ms_isometry"] for s in stats]))
     gem_ms = float(np.mean([s["ms_gemm"] for s in pst]))
@@ -287,6 +304,10 @@ def bench_ours(args, cfg):
                              "frac_of_fp64_peak": gem_fl / (t_c * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
                              "note": "isometries injected (INJECT_ISO): chains + corners + commit only, "
                                      "no reduced env, no SVD"},
+        "contraction_only_graph": {"moves_per_s": job_value(world, t_g), "ms_per_move": t_g,
+                                   "tflops": gem_fl / (t_g * 1e-3) / 1e12,
+                                   "frac_of_fp64_peak": gem_fl / (t_g * 1e-3) / 1e12 / FP64_PEAK_TFLOPS,
+                                   "note": "the same move captured once in a CUDA graph and replayed"},
 
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,

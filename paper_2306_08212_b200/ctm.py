@@ -168,11 +168,13 @@ class CtmHandle:
                                           _ptr(T3), mode, _ptr(M_out), _ptr(iso_out)))
         return M_out
 
-    def ctm_left_move(self, A, B, env, iso_in=None, iso_out=None):
+    def ctm_left_move(self, A, B, env, iso_in=None, iso_out=None, stats=True):
+        """stats=False passes no stats struct: the call then never synchronises the stream
+        (with iso_in and without CTM_FLAG_CHECK_FINITE it is capturable in a CUDA graph)."""
         st = ctm_move_stats()
         self._check(lib().ctm_left_move(self.h, _ptr(A), _ptr(B), byref(env.c), _ptr(iso_in), _ptr(iso_out),
-                                        byref(st)))
-        return st.as_dict()
+                                        byref(st) if stats else None))
+        return st.as_dict() if stats else None
 
     def ctm_move(self, direction, A, B, env):
         st = ctm_move_stats()

@@ -60,6 +60,24 @@ def run(name, steps, svd, strategy="sequential"):
             for _ in range(2):
                 step(True)
             con = [step(True) for _ in range(steps)]
+        ms_graph = None
+        if strategy == "sequential":
+            # contraction-only move replayed from a CUDA graph (SURVEY 8(d) timing protocol 3)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                h.ctm_left_move(A, B, env, iso_in=iso, stats=False)
+            graph.replay()
+            stream.synchronize()
+            ts = []
+            for _ in range(steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                graph.replay()
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            ms_graph = float(np.median(ts))
     F = ctm.ctm_move_flops(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp) if strategy == "sequential" else None
     Fc = con[0][1]["flops"]
     ms_full = float(np.median([t for t, _ in full]))
@@ -72,6 +90,8 @@ def run(name, steps, svd, strategy="sequential"):
             "contraction_only_ms": ms_con, "contraction_moves_per_s": 1e3 / ms_con,
             "contraction_tflops": Fc / (ms_con * 1e-3) / 1e12,
             "contraction_frac_of_fp64_peak": Fc / (ms_con * 1e-3) / 1e12 / PEAK,
+            "contraction_graph_ms": ms_graph,
+            "contraction_graph_frac_of_fp64_peak": (Fc / (ms_graph * 1e-3) / 1e12 / PEAK) if ms_graph else None,
             "peak_mem_gb": torch.cuda.max_memory_allocated() / 1e9}
 
 
