@@ -121,7 +121,9 @@ int chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
     double* b1 = h.ws.take(s1);
     double* b2 = h.ws.take(s2);
     X1[b] = {b1, {D, n1, D, D, cout}};
-    X2[b] = {b2, {n1, D, d, D, D, cout}};
+    // X2 stored (o, q, a, g, s, z): S3 contracts (q, o), its slowest legs, so S3's A tile is
+    // m-fast (a contiguous 128-element run) instead of k-fast
+    X2[b] = {b2, {D, cout, n1, D, d, D}};
     X3[b] = {b1, {n1, D, d, D, m1}};
     X4[b] = {b2, {d, D, D, D, m1, o1}};
     X5[b] = {b1, {m1, D, D, D, o1}};
@@ -146,11 +148,11 @@ int chain_batch(Handle& h, const std::vector<ChainJob>& jobs) {
   // S1: X1(i,a,f,g,q) = sum_p v1_in(p,i,a) T(p,f,g,q)                     K = chi
   contract(h, op(P([&](int b) { return &jobs[b].in->v1; }), "pia"), op(P([&](int b) { return jobs[b].T; }), "pfgq"),
            out(Q(X1), "iafgq"));
-  // S2: X2(a,g,s,z,o,q) = sum_{i,f} X1(i,a,f,g,q) X(i,f,s,o,z)               K = D^2
+  // S2: X2(o,q,a,g,s,z) = sum_{i,f} X1(i,a,f,g,q) X(i,f,s,o,z)               K = D^2
   contract(h, op(P([&](int b) { return (const Ten*)&X1[b]; }), "iafgq"),
-           op(P([&](int b) { return &jobs[b].X->ket; }), "ifsoz"), out(Q(X2), "agszoq"));
-  // S3: X3(a,g,s,z,b) = sum_{q,o} X2(a,g,s,z,o,q) v1_out(q,o,b)               K = chi D
-  contract(h, op(P([&](int b) { return (const Ten*)&X2[b]; }), "agszoq"),
+           op(P([&](int b) { return &jobs[b].X->ket; }), "ifsoz"), out(Q(X2), "oqagsz"));
+  // S3: X3(a,g,s,z,b) = sum_{q,o} X2(o,q,a,g,s,z) v1_out(q,o,b)               K = chi D
+  contract(h, op(P([&](int b) { return (const Ten*)&X2[b]; }), "oqagsz"),
            op(P([&](int b) { return &jobs[b].outv->v1; }), "qob"), out(Q(X3), "agszb"));
   // S4: X4(s,g,j,z,b,c) = sum_a X3(a,g,s,z,b) v2_in(a,j,c)                   K = chi'
   contract(h, op(P([&](int b) { return (const Ten*)&X3[b]; }), "agszb"),
