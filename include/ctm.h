@@ -78,8 +78,9 @@ extern "C" {
                                 with CholQR, Rayleigh-Ritz through a backward-stable QR and
                                 one-sided Jacobi (all libctm kernels + DMMA GEMMs); tall /
                                 small cuts: QR + one-sided Jacobi.  Shapes beyond its
-                                shared-memory limit (l > 160) or whose convergence it cannot
-                                certify fall back to Xgesvdp (counted in n_svd_fallback). */
+                                range (block l = n_keep + 32 > 320, or a tall/small cut wider
+                                than 320) or whose convergence it cannot certify fall back
+                                to Xgesvdp (counted in n_svd_fallback). */
 
 /* flags (ctm_params.flags) */
 #define CTM_FLAG_CHECK_FINITE 1   /* scan every committed tensor for NaN/Inf         */

@@ -23,7 +23,7 @@
 // rounding floor.  The sign rule (largest-|.| entry of each column positive) is applied by
 // the same extraction kernel the cuSOLVER path uses.
 //
-// Shapes this solver does not take (l > CTM_ISO_LMAX, or a rank-deficient keep with
+// Shapes this solver does not take (l > 2 CTM_ISO_LMAX, or a rank-deficient keep with
 // n > C) go to cuSOLVER gesvdp (svd.cu); there is no CPU path.
 #include <cmath>
 #include <cstdio>
@@ -60,10 +60,10 @@ struct Solver {
   unsigned seed = 0x9e3779b9u;
   explicit Solver(Handle& hh) : h(hh) {
     status = reinterpret_cast<int*>(h.ws.take(8));
-    repl = reinterpret_cast<int*>(h.ws.take(LMAX / 2 + 1));
+    repl = reinterpret_cast<int*>(h.ws.take(LMAX_BIG / 2 + 1));
     if (!h.dry) {
       CTM_CUDA(cudaMemsetAsync(status, 0, 8 * sizeof(double), h.stream));
-      CTM_CUDA(cudaMemsetAsync(repl, 0, LMAX * sizeof(int), h.stream));
+      CTM_CUDA(cudaMemsetAsync(repl, 0, LMAX_BIG * sizeof(int), h.stream));
     }
   }
   // C (m x n) = A * B with row-major operands given by label strings.
@@ -84,23 +84,71 @@ struct Solver {
     double* rd = h.ws.take((size_t)n);
     gemm(Y, "ia", {m, n}, Y, "ib", {m, n}, S, "ab", {n, n});
     if (h.dry) {
+      if (n > LMAX) chol_two_block(S, n, shift_factor, R, rd, replace);   // reserves its scratch
       h.ws.reset(mark);
       return;
     }
-    const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
-    chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
-                                                          replace ? repl : nullptr);
-    CTM_CUDA(cudaGetLastError());
-    const int rows_per_cta = 8;
-    const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
-    trsm_rows_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);
-    CTM_CUDA(cudaGetLastError());
-    h.count_kernel(2);
+    if (n <= LMAX) {
+      const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
+      chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
+                                                            replace ? repl : nullptr);
+      CTM_CUDA(cudaGetLastError());
+      h.count_kernel();
+    } else {
+      chol_two_block(S, n, shift_factor, R, rd, replace);
+    }
+    trsm(Y, m, n, R, rd, nullptr);
     if (replace) {
       replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
     }
+    h.ws.reset(mark);
+  }
+  void trsm(double* Y, int m, int n, const double* R, const double* rd, const int* dep) {
+    const int rows_per_cta = 8;
+    const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
+    if (n <= LMAX) trsm_rows_kernel<(LMAX + 31) / 32><<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd, dep);
+    else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+  }
+  // S (n x n, LMAX < n <= LMAX_BIG) + shift I = R^T R by two LMAX-sized blocks
+  // (chol_diag_shift_kernel's comment); same status / replacement conventions as chol_kernel.
+  void chol_two_block(double* S, int n, double shift_factor, double* R, double* rd, bool replace) {
+    const size_t mark = h.ws.top;
+    const int n1 = LMAX, n2 = n - n1;
+    double* dref = h.ws.take((size_t)n);
+    double* S11 = h.ws.take((size_t)n1 * n1);
+    double* W = h.ws.take((size_t)n2 * n1);
+    double* S22 = h.ws.take((size_t)n2 * n2);
+    double* R11 = h.ws.take((size_t)n1 * n1);
+    double* R22 = h.ws.take((size_t)n2 * n2);
+    if (h.dry) {
+      h.ws.reset(mark);
+      return;
+    }
+    const double tol = replace ? 1e-13 : 0.0;
+    chol_diag_shift_kernel<<<1, 256, 0, h.stream>>>(S, n, shift_factor, dref);
+    CTM_CUDA(cudaGetLastError());
+    const size_t sz = sizeof(double);
+    CTM_CUDA(cudaMemcpy2DAsync(S11, n1 * sz, S, n * sz, n1 * sz, n1, cudaMemcpyDeviceToDevice, h.stream));
+    CTM_CUDA(cudaMemcpy2DAsync(W, n1 * sz, S + (size_t)n1 * n, n * sz, n1 * sz, n2, cudaMemcpyDeviceToDevice, h.stream));
+    CTM_CUDA(cudaMemcpy2DAsync(S22, n2 * sz, S + (size_t)n1 * n + n1, n * sz, n2 * sz, n2, cudaMemcpyDeviceToDevice,
+                               h.stream));
+    const size_t smem1 = (size_t)n1 * ((n1 + 1) & ~1) * sz, smem2 = (size_t)n2 * ((n2 + 1) & ~1) * sz;
+    chol_kernel<<<1, CHOL_THREADS, smem1, h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
+                                                         dref);
+    CTM_CUDA(cudaGetLastError());
+    trsm(W, n2, n1, R11, rd, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
+    chol_schur_kernel<<<dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream>>>(S22, W, n2, n1);
+    CTM_CUDA(cudaGetLastError());
+    chol_kernel<<<1, CHOL_THREADS, smem2, h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
+                                                         replace ? repl + n1 : nullptr, dref + n1);
+    CTM_CUDA(cudaGetLastError());
+    chol_assemble_kernel<<<std::min(148, (n * n + 255) / 256), 256, 0, h.stream>>>(R, n, n1, R11, W, R22);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel(5);
     h.ws.reset(mark);
   }
   // passes of CholQR (the first one shifted when `shifted`), R_total = R_p ... R_1.
@@ -126,9 +174,13 @@ struct Solver {
     if (h.dry) return;
     const size_t smem = (size_t)n * (n + 1) * sizeof(double);
     int* st = max_sweeps < 0 ? status + 1 : status + 4;   // capped runs report into a scratch slot
-    if (n > 128) {   // register-resident 2-CTA cluster version: 1.4x faster per sweep at l = 160
-      jacobi_lsv2_kernel<<<2, jacobi2_threads(), jacobi2_smem_bytes(), h.stream>>>(
-          X, n, trans, ncols, U, S, st, max_sweeps < 0 ? 60 : max_sweeps, tol);
+    const int ms = max_sweeps < 0 ? 60 : max_sweeps;
+    if (n > LMAX) {   // C5: 8-CTA cluster, rows split eight ways
+      using J = JacCfg<8, 4, LMAX_BIG>;
+      jacobi_cluster_kernel<8, 4, LMAX_BIG><<<8, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol);
+    } else if (n > 128) {   // register-resident 2-CTA cluster: 1.4x faster per sweep at l = 160
+      using J = JacCfg<2, 8, LMAX>;
+      jacobi_cluster_kernel<2, 8, LMAX><<<2, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol);
     } else {
       jacobi_lsv_kernel<<<1, jacobi_threads(n), smem, h.stream>>>(X, n, trans, ncols, U, S, st,
                                                                   max_sweeps < 0 ? 60 : max_sweeps, tol);
@@ -155,16 +207,17 @@ void iso_init_kernels() {
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
   set_smem((const void*)chol_kernel, big);
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
-  set_smem((const void*)jacobi_lsv2_kernel, jacobi2_smem_bytes());
+  set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);
+  set_smem((const void*)jacobi_cluster_kernel<8, 4, LMAX_BIG>, JacCfg<8, 4, LMAX_BIG>::SMEM);
   done = true;
 }
 
 // Which path takes an R x C truncation to n_keep columns: 0 none (cuSOLVER), 1 direct tall
 // (R > C), 2 direct wide (R <= C, R small or no truncation), 3 subspace iteration.
 static int iso_plan(int R, int C, int n_keep) {
-  if (R > C) return (n_keep <= C && C <= LMAX) ? 1 : 0;   // n_keep > C: R11 null-space columns
-  if (n_keep == R || R <= n_keep + ISO_OVERSAMPLE) return R <= LMAX ? 2 : 0;
-  return n_keep + ISO_OVERSAMPLE <= LMAX ? 3 : 0;
+  if (R > C) return (n_keep <= C && C <= LMAX_BIG) ? 1 : 0;   // n_keep > C: R11 null-space columns
+  if (n_keep == R || R <= n_keep + ISO_OVERSAMPLE) return R <= LMAX_BIG ? 2 : 0;
+  return n_keep + ISO_OVERSAMPLE <= LMAX_BIG ? 3 : 0;
 }
 
 bool iso_supported(int R, int C, int n_keep) { return iso_plan(R, C, n_keep) != 0; }
@@ -344,8 +397,13 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
-    // (1e8 let the bottom columns of the block collapse numerically onto the top ones)
-    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(1e6) / (std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12))));
+    // (1e8 let the bottom columns of the block collapse numerically onto the top ones), and
+    // <= 0.25 / sqrt(shift): one shifted CholQR pass leaves kappa(Q) ~ sqrt(shift) kappa(Y),
+    // so a larger per-block spread compounds from block to block until kept directions
+    // drown (seen as Ritz residual blow-ups at l = 288).
+    const double shift_rel = 11.0 * ((double)R * l + (double)l * (l + 1)) * EPS;
+    const double spread = std::min(1e6, 0.25 / std::sqrt(shift_rel));
+    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / (std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12))));
     // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
     // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
     // (after the capped first check W is not orthogonal: keep filtering Y itself)
@@ -393,7 +451,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
 }
 
 // Singular values (descending) of a row-major R x C matrix into host memory: the one-sided
-// Jacobi kernels for square matrices up to LMAX, cuSOLVER Xgesvd (values only) otherwise.
+// Jacobi kernels for square matrices up to LMAX_BIG, cuSOLVER Xgesvd (values only) otherwise.
 void singular_values(Handle& h, const double* mat, int R, int C, double* host_out) {
   const size_t mark = h.ws.top;
   const int mn = std::min(R, C);
@@ -403,7 +461,7 @@ void singular_values(Handle& h, const double* mat, int R, int C, double* host_ou
     h.ws.reset(mark);
     return;
   }
-  if (R == C && R <= LMAX) {
+  if (R == C && R <= LMAX_BIG) {
     Solver sv(h);
     sv.jacobi(mat, R, 0, 0, nullptr, S, 1e-14);
     sv.check_status("singular values");

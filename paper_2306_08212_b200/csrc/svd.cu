@@ -217,6 +217,8 @@ double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* 
     }
     if (!h.dry) ++h.n_svd_fallback;   // not certified: the dense cuSOLVER factorisation below
     // (sizing pass: fall through so the workspace also covers the fallback)
+  } else if (h.prm.svd_algo == CTM_SVD_ISO && !h.dry) {
+    ++h.n_svd_fallback;   // shape outside the solver's range (l > 2 CTM_ISO_LMAX)
   }
   const Plan p = make_plan(R, C, n_keep);
   const int mn = std::min(p.m, p.n);

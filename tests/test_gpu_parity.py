@@ -141,7 +141,8 @@ def test_reduced_env_untruncated_equals_exact():
 # ----------------------------------------------------------------------------------------
 # rows a1-a11: left move; GPU isometries injected into the oracle -> entrywise parity
 # ----------------------------------------------------------------------------------------
-@pytest.mark.parametrize("name,svd", [(n, s) for n in ["tiny", "c2", "c3", "c4"] for s in SVDS] + [("c5", "iso")])
+@pytest.mark.parametrize("name,svd", [(n, s) for n in ["tiny", "c2", "c3", "c4"] for s in SVDS]
+                         + [("c5", "iso"), ("c5_256", "iso")])
 def test_left_move_entrywise_with_gpu_isometries(name, svd):
     cfg = ci.CONFIGS[name]
     g = ci.generate(cfg)
@@ -152,6 +153,8 @@ def test_left_move_entrywise_with_gpu_isometries(name, svd):
     st = h.ctm_left_move(T_(g["A"]), T_(g["B"]), env, iso_out=iso)
     # 12 per absorption, minus the right-side TS (2 x 2 SVDs) reused by the second one
     assert st["n_svd"] == 2 * 12 - 4 and np.isfinite(st["ms_total"])
+    if svd == "iso":   # every truncation (C5's l = 232 included) certified by libctm's solver
+        assert st["n_svd_fallback"] == 0
     got = env.to_host()
     projs = _iso_from_flat(iso.cpu().numpy(), cfg.chi, cfg.D, cfg.chi_p)
     e = {"C": g["C"], "T": g["T"]}

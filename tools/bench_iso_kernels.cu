@@ -69,6 +69,8 @@ int main(int argc, char** argv) {
     CK(cudaEventElapsedTime(&ms, e0, e1));
     return 1e3 * ms / reps;
   };
+  int st[4];
+  if (n <= LMAX) {   // one-CTA Cholesky + trsm at n <= LMAX
   // ---- Cholesky
   const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
   double us_chol = timeit([&]() { chol_kernel<<<1, CHOL_THREADS, smem_c>>>(dS, n, 0.0, dR, drd, dst); }, 20);
@@ -82,16 +84,15 @@ int main(int argc, char** argv) {
       err = std::max(err, std::fabs(t - S[(size_t)a * n + b]));
       nrm = std::max(nrm, std::fabs(S[(size_t)a * n + b]));
     }
-  int st[4];
   CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
   printf("{\"kernel\":\"chol\",\"n\":%d,\"us\":%.1f,\"rel_err\":%.3e,\"status\":%d}\n", n, us_chol, err / nrm, st[0]);
   // ---- triangular solve Y R^{-1}: then Q^T Q should be I
   double us_trsm = timeit([&]() {
     CK(cudaMemcpyAsync(dY, Y.data(), 0, cudaMemcpyHostToDevice));
-    trsm_rows_kernel<<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
+    trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
   }, 1);
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
-  trsm_rows_kernel<<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
+  trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
   CK(cudaGetLastError());
   std::vector<double> Q((size_t)m * n);
   CK(cudaMemcpy(Q.data(), dY, 8ull * m * n, cudaMemcpyDeviceToHost));
@@ -102,18 +103,25 @@ int main(int argc, char** argv) {
       for (int i = 0; i < m; ++i) t += Q[(size_t)i * n + a] * Q[(size_t)i * n + b];
       orth = std::max(orth, std::fabs(t - (a == b ? 1.0 : 0.0)));
     }
-  double us_trsm2 = timeit([&]() { trsm_rows_kernel<<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd); }, 20);
+  double us_trsm2 = timeit([&]() { trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd); }, 20);
   printf("{\"kernel\":\"trsm_rows\",\"m\":%d,\"n\":%d,\"us\":%.1f,\"orth_err\":%.3e}\n", m, n, us_trsm2, orth);
   (void)us_trsm;
+  }
   // ---- Jacobi on a random n x n matrix (X = R^T with trans = 1 means rows of R)
   std::vector<double> X((size_t)n * n);
   for (auto& v : X) v = urand(seed);
   CK(cudaMemcpy(dX, X.data(), 8ull * n * n, cudaMemcpyHostToDevice));
   const size_t smem_j = (size_t)n * (n + 1) * sizeof(double);
-  CK(cudaFuncSetAttribute(jacobi_lsv2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)jacobi2_smem_bytes()));
+  using J2 = JacCfg<2, 8, LMAX>;
+  using J4 = JacCfg<8, 4, LMAX_BIG>;
+  CK(cudaFuncSetAttribute(jacobi_cluster_kernel<2, 8, LMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J2::SMEM));
+  CK(cudaFuncSetAttribute(jacobi_cluster_kernel<8, 4, LMAX_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J4::SMEM));
   for (int sweeps : {1, 60}) {
     CK(cudaMemset(dst, 0, 64));
-    double us = timeit([&]() { jacobi_lsv2_kernel<<<2, jacobi2_threads(), jacobi2_smem_bytes()>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14); }, 3);
+    double us = timeit([&]() {
+      if (n > LMAX) jacobi_cluster_kernel<8, 4, LMAX_BIG><<<8, J4::THREADS, J4::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
+      else jacobi_cluster_kernel<2, 8, LMAX><<<2, J2::THREADS, J2::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
+    }, 3);
     CK(cudaGetLastError());
     CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
     std::vector<double> U((size_t)n * n), sig(n);
@@ -126,10 +134,11 @@ int main(int argc, char** argv) {
         for (int i = 0; i < n; ++i) t += U[(size_t)i * n + a] * U[(size_t)i * n + b];
         o = std::max(o, std::fabs(t - (a == b ? 1.0 : 0.0)));
       }
-    printf("{\"kernel\":\"jacobi2_cluster\",\"n\":%d,\"max_sweeps\":%d,\"sweeps\":%d,\"us\":%.1f,\"us_per_sweep\":%.1f,\"orth_err\":%.3e,\"s0\":%.6f,\"slast\":%.3e}\n",
+    printf("{\"kernel\":\"jacobi_cluster\",\"n\":%d,\"max_sweeps\":%d,\"sweeps\":%d,\"us\":%.1f,\"us_per_sweep\":%.1f,\"orth_err\":%.3e,\"s0\":%.6f,\"slast\":%.3e}\n",
            n, sweeps, st[2], us, us / std::max(1, st[2]), o, sig[0], sig[n - 1]);
   }
   for (int sweeps : {1, 60}) {
+    if (n > LMAX) break;   // one-CTA shared-memory Jacobi: n <= LMAX only
     for (double tol : {1e-14, 1e-8}) {
       if (sweeps == 1 && tol > 1e-10) continue;
       CK(cudaMemset(dst, 0, 64));
