@@ -82,6 +82,7 @@ struct Solver {
     const size_t mark = h.ws.top;
     double* S = h.ws.take((size_t)n * n);
     double* rd = h.ws.take((size_t)n);
+    double* Dinv = h.ws.take((size_t)(n + 31) / 32 * 32 * 32);
     gemm(Y, "ia", {m, n}, Y, "ib", {m, n}, S, "ab", {n, n});
     if (h.dry) {
       if (n > LMAX) chol_two_block(S, n, shift_factor, R, rd, replace);   // reserves its scratch
@@ -91,13 +92,13 @@ struct Solver {
     if (n <= LMAX) {
       const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
       chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
-                                                            replace ? repl : nullptr);
+                                                            replace ? repl : nullptr, nullptr, Dinv);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
     } else {
       chol_two_block(S, n, shift_factor, R, rd, replace);
     }
-    trsm(Y, m, n, R, rd, nullptr);
+    trsm(Y, m, n, R, rd, Dinv, nullptr);
     if (replace) {
       replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
       CTM_CUDA(cudaGetLastError());
@@ -105,10 +106,10 @@ struct Solver {
     }
     h.ws.reset(mark);
   }
-  void trsm(double* Y, int m, int n, const double* R, const double* rd, const int* dep) {
+  void trsm(double* Y, int m, int n, const double* R, const double* rd, const double* Dinv, const int* dep) {
     const int rows_per_cta = 8;
     const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
-    if (n <= LMAX) trsm_rows_kernel<(LMAX + 31) / 32><<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd, dep);
+    if (n <= LMAX) trsm_rows_kernel<(LMAX + 31) / 32><<<grid, 256, 0, h.stream>>>(Y, m, n, R, Dinv, dep);
     else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
@@ -124,6 +125,7 @@ struct Solver {
     double* S22 = h.ws.take((size_t)n2 * n2);
     double* R11 = h.ws.take((size_t)n1 * n1);
     double* R22 = h.ws.take((size_t)n2 * n2);
+    double* Dinv1 = h.ws.take((size_t)n1 * 32);
     if (h.dry) {
       h.ws.reset(mark);
       return;
@@ -138,9 +140,9 @@ struct Solver {
                                h.stream));
     const size_t smem1 = (size_t)n1 * ((n1 + 1) & ~1) * sz, smem2 = (size_t)n2 * ((n2 + 1) & ~1) * sz;
     chol_kernel<<<1, CHOL_THREADS, smem1, h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
-                                                         dref);
+                                                         dref, Dinv1);
     CTM_CUDA(cudaGetLastError());
-    trsm(W, n2, n1, R11, rd, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
+    trsm(W, n2, n1, R11, rd, Dinv1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
     chol_schur_kernel<<<dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream>>>(S22, W, n2, n1);
     CTM_CUDA(cudaGetLastError());
     chol_kernel<<<1, CHOL_THREADS, smem2, h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,

@@ -52,6 +52,8 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dU, 8ull * n * n));
   CK(cudaMalloc(&dSig, 8ull * n));
   CK(cudaMalloc(&dst, 64));
+  double* dDinv;
+  CK(cudaMalloc(&dDinv, 8ull * (LMAX_BIG + 32) * 32));
   CK(cudaMemset(dst, 0, 64));
   CK(cudaMemcpy(dS, S.data(), 8ull * n * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
@@ -73,7 +75,7 @@ int main(int argc, char** argv) {
   if (n <= LMAX) {   // one-CTA Cholesky + trsm at n <= LMAX
   // ---- Cholesky
   const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
-  double us_chol = timeit([&]() { chol_kernel<<<1, CHOL_THREADS, smem_c>>>(dS, n, 0.0, dR, drd, dst); }, 20);
+  double us_chol = timeit([&]() { chol_kernel<<<1, CHOL_THREADS, smem_c>>>(dS, n, 0.0, dR, drd, dst, 0.0, nullptr, nullptr, dDinv); }, 20);
   std::vector<double> R((size_t)n * n);
   CK(cudaMemcpy(R.data(), dR, 8ull * n * n, cudaMemcpyDeviceToHost));
   double err = 0, nrm = 0;
@@ -85,14 +87,30 @@ int main(int argc, char** argv) {
       nrm = std::max(nrm, std::fabs(S[(size_t)a * n + b]));
     }
   CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
+#ifdef CTM_CHOL_PROF
+  {
+    long long pr[64];
+    CK(cudaMemcpyFromSymbol(pr, chol_prof, sizeof(pr)));
+    printf("{\"chol_phase_cycles\": {");
+    long long prev = pr[0];
+    for (int b = 0; 32 * b < n; ++b)
+      for (int ph = 1; ph <= 3; ++ph) {
+        const long long t = pr[3 * b + ph];
+        if (32 * (b + 1) >= n && ph > 1) continue;
+        printf("\"b%d_%s\": %lld, ", b, ph == 1 ? "diag" : ph == 2 ? "panel" : "trail", t - prev);
+        prev = t;
+      }
+    printf("\"tail\": %lld, \"store\": %lld, \"dinv\": %lld}}\n", pr[40] - prev, pr[41] - pr[40], pr[42] - pr[41]);
+  }
+#endif
   printf("{\"kernel\":\"chol\",\"n\":%d,\"us\":%.1f,\"rel_err\":%.3e,\"status\":%d}\n", n, us_chol, err / nrm, st[0]);
   // ---- triangular solve Y R^{-1}: then Q^T Q should be I
   double us_trsm = timeit([&]() {
     CK(cudaMemcpyAsync(dY, Y.data(), 0, cudaMemcpyHostToDevice));
-    trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
+    trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv);
   }, 1);
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
-  trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd);
+  trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv);
   CK(cudaGetLastError());
   std::vector<double> Q((size_t)m * n);
   CK(cudaMemcpy(Q.data(), dY, 8ull * m * n, cudaMemcpyDeviceToHost));
@@ -103,7 +121,7 @@ int main(int argc, char** argv) {
       for (int i = 0; i < m; ++i) t += Q[(size_t)i * n + a] * Q[(size_t)i * n + b];
       orth = std::max(orth, std::fabs(t - (a == b ? 1.0 : 0.0)));
     }
-  double us_trsm2 = timeit([&]() { trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, drd); }, 20);
+  double us_trsm2 = timeit([&]() { trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv); }, 20);
   printf("{\"kernel\":\"trsm_rows\",\"m\":%d,\"n\":%d,\"us\":%.1f,\"orth_err\":%.3e}\n", m, n, us_trsm2, orth);
   (void)us_trsm;
   }
