@@ -78,11 +78,14 @@ struct Solver {
   // One CholQR pass on Y (m x n): S = Y^T Y, S (+shift) = R^T R, Y <- Y R^{-1}.
   // replace: numerically dependent columns (pivot <= 1e-13 of the column's squared norm)
   // are overwritten with random directions instead of failing; a later pass re-orthonormalises.
-  void cholqr_pass(double* Y, int m, int n, double shift_factor, double* R, bool replace = false) {
+  // also (optional, m x n): right-multiplied by the same R^{-1} (keeps a three-term
+  // recurrence consistent across the orthonormalisation).
+  void cholqr_pass(double* Y, int m, int n, double shift_factor, double* R, bool replace = false,
+                   double* also = nullptr) {
     const size_t mark = h.ws.top;
     double* S = h.ws.take((size_t)n * n);
     double* rd = h.ws.take((size_t)n);
-    double* Dinv = h.ws.take((size_t)(n + 31) / 32 * 32 * 32);
+    double* Rpk = n <= LMAX ? h.ws.take(rpk_size(n)) : nullptr;
     gemm(Y, "ia", {m, n}, Y, "ib", {m, n}, S, "ab", {n, n});
     if (h.dry) {
       if (n > LMAX) chol_two_block(S, n, shift_factor, R, rd, replace);   // reserves its scratch
@@ -92,13 +95,14 @@ struct Solver {
     if (n <= LMAX) {
       const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
       chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
-                                                            replace ? repl : nullptr, nullptr, Dinv);
+                                                            replace ? repl : nullptr, nullptr, Rpk);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
     } else {
       chol_two_block(S, n, shift_factor, R, rd, replace);
     }
-    trsm(Y, m, n, R, rd, Dinv, nullptr);
+    trsm(Y, m, n, R, rd, Rpk, nullptr);
+    if (also) trsm(also, m, n, R, rd, Rpk, nullptr);
     if (replace) {
       replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
       CTM_CUDA(cudaGetLastError());
@@ -106,10 +110,12 @@ struct Solver {
     }
     h.ws.reset(mark);
   }
-  void trsm(double* Y, int m, int n, const double* R, const double* rd, const double* Dinv, const int* dep) {
+  void trsm(double* Y, int m, int n, const double* R, const double* rd, const double* Rpk, const int* dep) {
     const int rows_per_cta = 8;
     const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
-    if (n <= LMAX) trsm_rows_kernel<(LMAX + 31) / 32><<<grid, 256, 0, h.stream>>>(Y, m, n, R, Dinv, dep);
+    if (n <= LMAX)
+      trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(grid, 148), 256, rpk_size(n) * sizeof(double), h.stream>>>(
+          Y, m, n, Rpk, dep);
     else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
@@ -125,7 +131,7 @@ struct Solver {
     double* S22 = h.ws.take((size_t)n2 * n2);
     double* R11 = h.ws.take((size_t)n1 * n1);
     double* R22 = h.ws.take((size_t)n2 * n2);
-    double* Dinv1 = h.ws.take((size_t)n1 * 32);
+    double* Rpk1 = h.ws.take(rpk_size(n1));
     if (h.dry) {
       h.ws.reset(mark);
       return;
@@ -140,9 +146,9 @@ struct Solver {
                                h.stream));
     const size_t smem1 = (size_t)n1 * ((n1 + 1) & ~1) * sz, smem2 = (size_t)n2 * ((n2 + 1) & ~1) * sz;
     chol_kernel<<<1, CHOL_THREADS, smem1, h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
-                                                         dref, Dinv1);
+                                                         dref, Rpk1);
     CTM_CUDA(cudaGetLastError());
-    trsm(W, n2, n1, R11, rd, Dinv1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
+    trsm(W, n2, n1, R11, rd, Rpk1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
     chol_schur_kernel<<<dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream>>>(S22, W, n2, n1);
     CTM_CUDA(cudaGetLastError());
     chol_kernel<<<1, CHOL_THREADS, smem2, h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
@@ -154,14 +160,15 @@ struct Solver {
     h.ws.reset(mark);
   }
   // passes of CholQR (the first one shifted when `shifted`), R_total = R_p ... R_1.
-  void cholqr(double* Y, int m, int n, int passes, bool shifted, double* Rtot, bool replace = false) {
+  void cholqr(double* Y, int m, int n, int passes, bool shifted, double* Rtot, bool replace = false,
+              double* also = nullptr) {
     const size_t mark = h.ws.top;
     double* R = h.ws.take((size_t)n * n);
     double* T = Rtot ? h.ws.take((size_t)n * n) : nullptr;
     for (int p = 0; p < passes; ++p) {
       const double sf = (shifted && p == 0) ? 11.0 * ((double)m * n + (double)n * (n + 1)) * EPS : 0.0;
       double* Rp = (Rtot && p == 0) ? Rtot : R;
-      cholqr_pass(Y, m, n, sf, Rp, replace && p == 1);   // the first plain pass may replace columns
+      cholqr_pass(Y, m, n, sf, Rp, replace && p == 1, passes == 1 ? also : nullptr);   // the first plain pass may replace columns
       if (Rtot && p > 0) {   // Rtot <- R_p Rtot
         gemm(R, "ab", {n, n}, Rtot, "bc", {n, n}, T, "ac", {n, n});
         if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Rtot, T, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, h.stream));
@@ -208,6 +215,7 @@ void iso_init_kernels() {
   if (done) return;
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
   set_smem((const void*)chol_kernel, big);
+  set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
   set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<8, 4, LMAX_BIG>, JacCfg<8, 4, LMAX_BIG>::SMEM);
@@ -395,7 +403,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     const double rate = xk + std::sqrt(xk * xk - 1.0);
     // the first estimate comes from a young subspace (Ritz values of the block bottom are
     // low, the rate optimistic): over-filter by 1.6x rather than pay another check
-    const double safety = 1.25;
+    const double safety = std::getenv("CTM_ISO_SAFETY") ? std::atof(std::getenv("CTM_ISO_SAFETY")) : 1.25;
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
@@ -410,19 +418,24 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
     // (after the capped first check W is not orthogonal: keep filtering Y itself)
     if (checks > 1) CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
-    int done = 0;
+    // One Chebyshev recurrence over all `need` degrees; every mb degrees the current iterate
+    // is re-orthonormalised (shifted CholQR, a basis is enough here) and the previous one is
+    // multiplied by the same R^{-1}, so the three-term recurrence continues across the
+    // orthonormalisation (restarting it at T_1 would give the shifted-power rate x_k per
+    // degree instead of x_k + sqrt(x_k^2 - 1) on the steep cuts, where mb = 1).
+    const double s1 = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
+    static const int cont_min = std::getenv("CTM_ISO_CONT_MIN") ? std::atoi(std::getenv("CTM_ISO_CONT_MIN")) : 2;
+    double sig = s1;
+    double *Yo = nullptr, *Yc = Y;
+    double* bufs[2] = {Y1, Y2};
+    int nb = 0, done = 0;
     while (done < need) {
       const int m = std::min(mb, need - done);
-      const double s1 = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
-      double sig = s1;
-      double *Yo = nullptr, *Yc = Y;
-      double* bufs[2] = {Y1, Y2};
-      int nb = 0;
       for (int j = 0; j < m; ++j) {
         GYf(Yc, P);
         double* Yn = bufs[nb];
         nb ^= 1;
-        if (j == 0) {
+        if (Yo == nullptr) {
           combine(Yn, P, Yc, nullptr, s1 / ce, -s1, 0.0);
         } else {
           const double sn = 1.0 / (2.0 / s1 - sig);
@@ -432,10 +445,15 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
       }
-      if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
-      sv.cholqr(Y, R, l, 1, true, nullptr);   // shifted: a basis is enough between filter blocks
+      // (cont_min: continue the recurrence only when a block spans >= cont_min degrees --
+      // with mb = 1 the extra solve on Yo costs more than the faster rate saves at C4)
+      const bool cont = mb >= cont_min;
+      sv.cholqr(Yc, R, l, 1, true, nullptr, false, cont ? Yo : nullptr);
+      if (!cont) Yo = nullptr;   // restart at T_1 (sig re-initialised below)
+      if (!cont) sig = s1;
       done += m;
     }
+    if (!h.dry && Yc != Y) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
     degrees += need;
   }
   if (debug) {

@@ -53,7 +53,8 @@ int main(int argc, char** argv) {
   CK(cudaMalloc(&dSig, 8ull * n));
   CK(cudaMalloc(&dst, 64));
   double* dDinv;
-  CK(cudaMalloc(&dDinv, 8ull * (LMAX_BIG + 32) * 32));
+  CK(cudaMalloc(&dDinv, 8ull * rpk_size(LMAX)));
+  CK(cudaFuncSetAttribute(trsm_rows_kernel<(LMAX + 31) / 32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * rpk_size(LMAX))));
   CK(cudaMemset(dst, 0, 64));
   CK(cudaMemcpy(dS, S.data(), 8ull * n * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
@@ -107,10 +108,10 @@ int main(int argc, char** argv) {
   // ---- triangular solve Y R^{-1}: then Q^T Q should be I
   double us_trsm = timeit([&]() {
     CK(cudaMemcpyAsync(dY, Y.data(), 0, cudaMemcpyHostToDevice));
-    trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv);
+    trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(148, (m + 7) / 8), 256, 8 * rpk_size(n)>>>(dY, m, n, dDinv);
   }, 1);
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
-  trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv);
+  trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(148, (m + 7) / 8), 256, 8 * rpk_size(n)>>>(dY, m, n, dDinv);
   CK(cudaGetLastError());
   std::vector<double> Q((size_t)m * n);
   CK(cudaMemcpy(Q.data(), dY, 8ull * m * n, cudaMemcpyDeviceToHost));
@@ -121,7 +122,7 @@ int main(int argc, char** argv) {
       for (int i = 0; i < m; ++i) t += Q[(size_t)i * n + a] * Q[(size_t)i * n + b];
       orth = std::max(orth, std::fabs(t - (a == b ? 1.0 : 0.0)));
     }
-  double us_trsm2 = timeit([&]() { trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(4 * 148, (m + 7) / 8), 256>>>(dY, m, n, dR, dDinv); }, 20);
+  double us_trsm2 = timeit([&]() { trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(148, (m + 7) / 8), 256, 8 * rpk_size(n)>>>(dY, m, n, dDinv); }, 20);
   printf("{\"kernel\":\"trsm_rows\",\"m\":%d,\"n\":%d,\"us\":%.1f,\"orth_err\":%.3e}\n", m, n, us_trsm2, orth);
   (void)us_trsm;
   }
