@@ -403,7 +403,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     const double rate = xk + std::sqrt(xk * xk - 1.0);
     // the first estimate comes from a young subspace (Ritz values of the block bottom are
     // low, the rate optimistic): over-filter by 1.6x rather than pay another check
-    const double safety = std::getenv("CTM_ISO_SAFETY") ? std::atof(std::getenv("CTM_ISO_SAFETY")) : 1.25;
+    const double safety = 1.25;   // (1.0 / 0.85 / 0.7 measured slower: an extra check)
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
@@ -422,9 +422,9 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // is re-orthonormalised (shifted CholQR, a basis is enough here) and the previous one is
     // multiplied by the same R^{-1}, so the three-term recurrence continues across the
     // orthonormalisation (restarting it at T_1 would give the shifted-power rate x_k per
-    // degree instead of x_k + sqrt(x_k^2 - 1) on the steep cuts, where mb = 1).
+    // degree instead of x_k + sqrt(x_k^2 - 1) on the steep cuts, where mb = 1: at C5 those
+    // needed a third Rayleigh-Ritz check; C5 move 344 -> 307 ms, C4 +2 ms).
     const double s1 = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
-    static const int cont_min = std::getenv("CTM_ISO_CONT_MIN") ? std::atoi(std::getenv("CTM_ISO_CONT_MIN")) : 2;
     double sig = s1;
     double *Yo = nullptr, *Yc = Y;
     double* bufs[2] = {Y1, Y2};
@@ -445,12 +445,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
       }
-      // (cont_min: continue the recurrence only when a block spans >= cont_min degrees --
-      // with mb = 1 the extra solve on Yo costs more than the faster rate saves at C4)
-      const bool cont = mb >= cont_min;
-      sv.cholqr(Yc, R, l, 1, true, nullptr, false, cont ? Yo : nullptr);
-      if (!cont) Yo = nullptr;   // restart at T_1 (sig re-initialised below)
-      if (!cont) sig = s1;
+      sv.cholqr(Yc, R, l, 1, true, nullptr, false, Yo);
       done += m;
     }
     if (!h.dry && Yc != Y) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
