@@ -93,8 +93,7 @@ struct Solver {
       return;
     }
     if (n <= LMAX) {
-      const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
-      chol_kernel<<<1, CHOL_THREADS, smem_c, h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
+      chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n), h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
                                                             replace ? repl : nullptr, nullptr, Rpk);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
@@ -144,14 +143,13 @@ struct Solver {
     CTM_CUDA(cudaMemcpy2DAsync(W, n1 * sz, S + (size_t)n1 * n, n * sz, n1 * sz, n2, cudaMemcpyDeviceToDevice, h.stream));
     CTM_CUDA(cudaMemcpy2DAsync(S22, n2 * sz, S + (size_t)n1 * n + n1, n * sz, n2 * sz, n2, cudaMemcpyDeviceToDevice,
                                h.stream));
-    const size_t smem1 = (size_t)n1 * ((n1 + 1) & ~1) * sz, smem2 = (size_t)n2 * ((n2 + 1) & ~1) * sz;
-    chol_kernel<<<1, CHOL_THREADS, smem1, h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
+    chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n1), h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
                                                          dref, Rpk1);
     CTM_CUDA(cudaGetLastError());
     trsm(W, n2, n1, R11, rd, Rpk1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
     chol_schur_kernel<<<dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream>>>(S22, W, n2, n1);
     CTM_CUDA(cudaGetLastError());
-    chol_kernel<<<1, CHOL_THREADS, smem2, h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
+    chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n2), h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
                                                          replace ? repl + n1 : nullptr, dref + n1);
     CTM_CUDA(cudaGetLastError());
     chol_assemble_kernel<<<std::min(148, (n * n + 255) / 256), 256, 0, h.stream>>>(R, n, n1, R11, W, R22);
@@ -214,7 +212,7 @@ void iso_init_kernels() {
   static bool done = false;
   if (done) return;
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
-  set_smem((const void*)chol_kernel, big);
+  set_smem((const void*)chol_kernel, chol_smem_bytes(LMAX));
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
   set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);

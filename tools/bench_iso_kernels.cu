@@ -75,7 +75,7 @@ int main(int argc, char** argv) {
   int st[4];
   if (n <= LMAX) {   // one-CTA Cholesky + trsm at n <= LMAX
   // ---- Cholesky
-  const size_t smem_c = (size_t)n * ((n + 1) & ~1) * sizeof(double);
+  const size_t smem_c = chol_smem_bytes(n);
   double us_chol = timeit([&]() { chol_kernel<<<1, CHOL_THREADS, smem_c>>>(dS, n, 0.0, dR, drd, dst, 0.0, nullptr, nullptr, dDinv); }, 20);
   std::vector<double> R((size_t)n * n);
   CK(cudaMemcpy(R.data(), dR, 8ull * n * n, cudaMemcpyDeviceToHost));
@@ -101,7 +101,7 @@ int main(int argc, char** argv) {
         printf("\"b%d_%s\": %lld, ", b, ph == 1 ? "diag" : ph == 2 ? "panel" : "trail", t - prev);
         prev = t;
       }
-    printf("\"tail\": %lld, \"store\": %lld, \"dinv\": %lld}}\n", pr[40] - prev, pr[41] - pr[40], pr[42] - pr[41]);
+    printf("\"tail\": %lld, \"store\": %lld, \"pack\": %lld, \"dinv\": %lld}}\n", pr[40] - prev, pr[41] - pr[40], pr[43] - pr[41], pr[42] - pr[43]);
   }
 #endif
   printf("{\"kernel\":\"chol\",\"n\":%d,\"us\":%.1f,\"rel_err\":%.3e,\"status\":%d}\n", n, us_chol, err / nrm, st[0]);
