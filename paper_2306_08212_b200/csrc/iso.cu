@@ -188,12 +188,33 @@ struct Solver {
     } else if (n > 128) {   // register-resident 2-CTA cluster: 1.4x faster per sweep at l = 160
       using J = JacCfg<2, 8, LMAX>;
       jacobi_cluster_kernel<2, 8, LMAX><<<2, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol);
+    } else if (n > 32 && !std::getenv("CTM_ISO_JAC_SMEM")) {   // register-resident, one CTA
+      using J = JacCfg<1, 8, 128>;
+      jacobi_cluster_kernel<1, 8, 128><<<1, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol);
     } else {
       jacobi_lsv_kernel<<<1, jacobi_threads(n), smem, h.stream>>>(X, n, trans, ncols, U, S, st,
                                                                   max_sweeps < 0 ? 60 : max_sweeps, tol);
     }
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
+  }
+  // Preconditioned one-sided Jacobi (Drmac & Veselic): the left singular vectors of
+  // Xc = (trans ? X^T : X) (n x n) equal those of R'^T where Xc^T = Q R' (sCholQR3; the
+  // right factor Q^T drops out), and the columns of R'^T are far closer to orthogonal --
+  // R' R'^T = Q^T (Xc^T Xc) Q is one step of the LR iteration on the Gram -- so the
+  // Jacobi needs fewer sweeps.  Same outputs as jacobi(X, n, trans, ...).
+  void jacobi_pc(const double* X, int n, int trans, int ncols, double* U, double* S, double tol = 1e-14,
+                 int max_sweeps = -1) {
+    const size_t mark = h.ws.top;
+    double* T = h.ws.take((size_t)n * n);
+    double* Rp = h.ws.take((size_t)n * n);
+    if (!h.dry) {
+      if (trans) CTM_CUDA(cudaMemcpyAsync(T, X, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, h.stream));
+      else permute(h, X, {n, n}, {1, 0}, T);   // T = Xc^T
+    }
+    cholqr(T, n, n, 3, true, Rp);
+    jacobi(Rp, n, 1, ncols, U, S, tol, max_sweeps);
+    h.ws.reset(mark);
   }
   void check_status(const char* what) {
     if (h.dry) return;
@@ -216,6 +237,7 @@ void iso_init_kernels() {
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
   set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);
+  set_smem((const void*)jacobi_cluster_kernel<1, 8, 128>, JacCfg<1, 8, 128>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<8, 4, LMAX_BIG>, JacCfg<8, 4, LMAX_BIG>::SMEM);
   done = true;
 }
@@ -229,6 +251,11 @@ static int iso_plan(int R, int C, int n_keep) {
 }
 
 bool iso_supported(int R, int C, int n_keep) { return iso_plan(R, C, n_keep) != 0; }
+
+static bool debug_direct() {
+  static const bool d = std::getenv("CTM_ISO_DEBUG") != nullptr;
+  return d;
+}
 
 // First n_keep left singular vectors of the row-major R x C matrix `mat` (sign rule
 // applied), written row-major (R, n_keep) into `out`.  Returns sigma_n / sigma_{n+1}
@@ -256,11 +283,17 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       else permute(h, mat, {R, C}, {1, 0}, Y);   // M^T (C x R)
     }
     sv.cholqr(Y, tall ? R : C, n, 3, true, Rm);
-    sv.jacobi(Rm, n, tall ? 0 : 1, n, W, S);
+    static const bool no_pc = std::getenv("CTM_ISO_NOPC") != nullptr;
+    if (no_pc) sv.jacobi(Rm, n, tall ? 0 : 1, n, W, S);
+    else sv.jacobi_pc(Rm, n, tall ? 0 : 1, n, W, S);
     ++h.n_svd;
     if (h.dry) {
       h.ws.reset(mark);
       return inf;
+    }
+    if (debug_direct()) {
+      sv.check_status("iso direct");
+      std::fprintf(stderr, "[iso] direct %d x %d keep %d: n=%d jacobi sweeps %d\n", R, C, n_keep, n, sv.last_sweeps);
     }
     const double* U = W;
     if (tall) {

@@ -134,12 +134,15 @@ int main(int argc, char** argv) {
   using J2 = JacCfg<2, 8, LMAX>;
   using J4 = JacCfg<8, 4, LMAX_BIG>;
   CK(cudaFuncSetAttribute(jacobi_cluster_kernel<2, 8, LMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J2::SMEM));
+  using J1 = JacCfg<1, 8, 128>;
+  CK(cudaFuncSetAttribute(jacobi_cluster_kernel<1, 8, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J1::SMEM));
   CK(cudaFuncSetAttribute(jacobi_cluster_kernel<8, 4, LMAX_BIG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)J4::SMEM));
   for (int sweeps : {1, 60}) {
     CK(cudaMemset(dst, 0, 64));
     double us = timeit([&]() {
       if (n > LMAX) jacobi_cluster_kernel<8, 4, LMAX_BIG><<<8, J4::THREADS, J4::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
-      else jacobi_cluster_kernel<2, 8, LMAX><<<2, J2::THREADS, J2::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
+      else if (n > 128) jacobi_cluster_kernel<2, 8, LMAX><<<2, J2::THREADS, J2::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
+      else jacobi_cluster_kernel<1, 8, 128><<<1, J1::THREADS, J1::SMEM>>>(dX, n, 1, n, dU, dSig, dst + 1, sweeps, 1e-14);
     }, 3);
     CK(cudaGetLastError());
     CK(cudaMemcpy(st, dst, 16, cudaMemcpyDeviceToHost));
