@@ -374,7 +374,6 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     sv.cholqr(Y, R, l, 3, true, nullptr, true);   // sCholQR3 (dependent columns replaced): orthonormal
     GY(Y, P);
     sv.cholqr(Z, C, l, 2, true, Rz);         // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR2)
-    // the first Rayleigh-Ritz only estimates the spectrum for the filter: loose Jacobi
     // the first Rayleigh-Ritz only seeds the filter bounds: a capped, loose Jacobi suffices
     // (one sweep: C4 74.5 -> 71 ms vs three; zero sweeps -- column norms only -- mis-set the
     // C5 filter bounds and cost a fallback)
