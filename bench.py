@@ -219,7 +219,16 @@ def bench_ours(args, cfg):
         if world > 1:
             torch.distributed.barrier()
         with ClockSampler(local) as clk:
-            ms = [step(stats=stats) for _ in range(args.steps)]
+            ms = []
+            for i in range(args.steps):
+                # CTM_BENCH_PROFILE=1: ncu --profile-from-start off captures the first timed step
+                # (the launch list under profiles/ comes from this command)
+                prof = i == 0 and os.environ.get("CTM_BENCH_PROFILE") == "1"
+                if prof:
+                    torch.cuda.profiler.start()
+                ms.append(step(stats=stats))
+                if prof:
+                    torch.cuda.profiler.stop()
         torch.cuda.synchronize()
         launches = h.kernel_count - k0
         # contraction-only (isometries injected: no reduced env, no SVD) -- the hot contraction
