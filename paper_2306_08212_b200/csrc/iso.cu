@@ -38,7 +38,11 @@ namespace ctm {
 namespace {
 
 using namespace isok;
-constexpr int ISO_OVERSAMPLE = 32;
+// Block oversampling p (l = n + p): 32, or 48 when l exceeds the one-CTA limit LMAX anyway
+// (C5: 284 -> 269 ms per move; 16 / 24 were slower at C4, 48 / 64 at C4 cross the LMAX cliff).
+static int iso_oversample(int n_keep) {
+  return (n_keep + 32 > LMAX && n_keep + 48 <= LMAX_BIG) ? 48 : 32;
+}
 constexpr double EPS = 2.220446049250313e-16;
 
 // ---------------------------------------------------------------------------------------
@@ -246,8 +250,8 @@ void iso_init_kernels() {
 // (R > C), 2 direct wide (R <= C, R small or no truncation), 3 subspace iteration.
 static int iso_plan(int R, int C, int n_keep) {
   if (R > C) return (n_keep <= C && C <= LMAX_BIG) ? 1 : 0;   // n_keep > C: R11 null-space columns
-  if (n_keep == R || R <= n_keep + ISO_OVERSAMPLE) return R <= LMAX_BIG ? 2 : 0;
-  return n_keep + ISO_OVERSAMPLE <= LMAX_BIG ? 3 : 0;
+  if (n_keep == R || R <= n_keep + 32) return R <= LMAX_BIG ? 2 : 0;
+  return n_keep + 32 <= LMAX_BIG ? 3 : 0;
 }
 
 bool iso_supported(int R, int C, int n_keep) { return iso_plan(R, C, n_keep) != 0; }
@@ -313,7 +317,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     return gap;
   }
   // truncating cut: Chebyshev-filtered subspace iteration with Rayleigh-Ritz
-  const int l = std::min(n_keep + ISO_OVERSAMPLE, R);
+  const int l = std::min(n_keep + iso_oversample(n_keep), R);
   const int k = n_keep;
   double* Y = h.ws.take((size_t)R * l);
   double* Y1 = h.ws.take((size_t)R * l);
@@ -357,7 +361,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   }
   sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
   sv.cholqr(Y, R, l, 1, true, nullptr);
-  for (int it = 0; it < 4; ++it) {
+  for (int it = 0; it < 4; ++it) {   // (2 or 6 steps: slower at C5 / C4)
     GY(Y, P);
     std::swap(Y, P);
     sv.cholqr(Y, R, l, 1, true, nullptr);
