@@ -35,6 +35,7 @@ import numpy as np  # noqa: E402
 import ctm_inputs as ci  # noqa: E402
 
 FP64_PEAK_TFLOPS = 37.14   # measured DMMA.8x8x4 loop peak on this pool's B200 (profiles/r01_probe_fp64.txt)
+FP64_DFMA_PEAK_TFLOPS = 36.93   # measured DFMA loop peak, same file
 METRIC = "CTM moves/sec and FP64 TFLOP/s (% of B200 FP64 peak) vs D,chi"
 
 
@@ -295,6 +296,10 @@ def bench_ours(args, cfg):
     gem_fl = float(np.mean([s["gemm_flops"] for s in pst]))
     gem_n = float(np.mean([s["gemm_launches"] for s in pst]))
     achieved = gem_fl / (gem_ms * 1e-3) / 1e12
+    jac_ms = float(np.mean([s["ms_jacobi"] for s in stats]))
+    jac_fl = float(np.mean([s["jacobi_flops"] for s in stats]))
+    jac_n = float(np.mean([s["n_jacobi"] for s in stats]))
+    jac_achieved = jac_fl / (jac_ms * 1e-3) / 1e12 if jac_ms > 0 else None
     if rank != 0:
         return
     value = job_value(world, t_step)
@@ -320,7 +325,18 @@ def bench_ours(args, cfg):
 
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
-        "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4)", "achieved": achieved,
+        # the dominant kernel family of the step by device time (profiles/r01_final_ncu_launches_bench_step.txt:
+        # Jacobi 33%, Cholesky 28%, tc_gemm 23%): the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA
+        # cores, latency/issue-bound on 1-8 CTAs per launch; timed by CUDA events on the worker streams
+        "roofline": ({"bound": "alu", "kernel": "jacobi_cluster_kernel (one-sided Jacobi, FP64 DFMA)",
+                      "achieved": jac_achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                      "frac": jac_achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
+                      "launches_per_step": jac_n, "ms_per_step": jac_ms, "flops_per_step": jac_fl,
+                      "flops_unit": "6 n^2 (n-1) per executed sweep",
+                      "peak_source": "measured DFMA loop, whole GPU (profiles/r01_probe_fp64.txt); one launch "
+                                     "occupies 1-8 SMs, whose share of that peak is 1-8 x 0.25 TFLOP/s"}
+                     if jac_achieved else None),
+        "roofline_contraction": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4)", "achieved": achieved,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                      "traffic": traffic_bytes(cfg), "traffic_unit": "DRAM bytes per step (ncu, profiles/r01_final_traffic.json)",
                      "launches_per_step": gem_n, "ms_per_step": gem_ms,

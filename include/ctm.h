@@ -144,6 +144,12 @@ typedef struct {
   double ms_isometry;   /* wall device time of the isometry stages (reduced envs + TS,  */
                         /* rows a1-a5) on the caller's stream, fork to join            */
   int n_svd_fallback;   /* CTM_SVD_ISO truncations that fell back to cuSOLVER Xgesvdp   */
+  /* CTM_SVD_ISO: the one-sided Jacobi SVD launches of the solver, timed by CUDA events on
+     their (worker) streams; flops = 6 n^2 (n - 1) per executed sweep (per rotation pair and
+     round: three inner products, 6n, and the rotation, 6n)                                 */
+  double ms_jacobi;     /* summed device time of the Jacobi launches                    */
+  double jacobi_flops;  /* their algorithmic flops                                       */
+  int n_jacobi;         /* number of Jacobi launches                                     */
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by

@@ -291,6 +291,9 @@ void sub_begin(Handle& s) {
   s.min_gap = std::numeric_limits<double>::infinity();
   s.n_svd = 0;
   s.n_svd_fallback = 0;
+  s.ms_jacobi = 0.0;
+  s.jacobi_flops = 0.0;
+  s.n_jacobi = 0;
   s.n_kernels = 0;
   s.dry = false;
 }
@@ -300,6 +303,9 @@ void sub_merge(Handle& h, Handle& s) {
   h.min_gap = std::min(h.min_gap, s.min_gap);
   h.n_svd += s.n_svd;
   h.n_svd_fallback += s.n_svd_fallback;
+  h.ms_jacobi += s.ms_jacobi;
+  h.jacobi_flops += s.jacobi_flops;
+  h.n_jacobi += s.n_jacobi;
   h.n_kernels += s.n_kernels;
   h.kernel_count += s.n_kernels;
 }
@@ -1069,6 +1075,9 @@ void begin_call(Handle& h) {
   h.min_gap = std::numeric_limits<double>::infinity();
   h.n_svd = 0;
   h.n_svd_fallback = 0;
+  h.ms_jacobi = 0.0;
+  h.jacobi_flops = 0.0;
+  h.n_jacobi = 0;
   h.n_kernels = 0;
   h.prof_used = 0;
   if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
@@ -1085,6 +1094,9 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->min_gap = h.min_gap;
   st->n_svd = h.n_svd;
   st->n_svd_fallback = h.n_svd_fallback;
+  st->ms_jacobi = h.ms_jacobi;
+  st->jacobi_flops = h.jacobi_flops;
+  st->n_jacobi = h.n_jacobi;
   st->n_kernels = h.n_kernels;
   st->ms_gemm = 0.0;
   st->gemm_flops = 0.0;
@@ -1187,6 +1199,7 @@ void init_solver(Handle& h, const ctm_params* p) {
   CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
   h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
   for (auto& e : h.ev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
+  for (auto& e : h.jev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
 }
 
 void destroy_handle(Handle& h) {
@@ -1196,6 +1209,8 @@ void destroy_handle(Handle& h) {
   if (h.solver_params) cusolverDnDestroyParams(h.solver_params);
   if (h.solver) cusolverDnDestroy(h.solver);
   for (auto& e : h.ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : h.jev)
     if (e) cudaEventDestroy(e);
   for (auto& e : h.prof_ev) cudaEventDestroy(e);
   if (h.dev_scalars) cudaFree(h.dev_scalars);

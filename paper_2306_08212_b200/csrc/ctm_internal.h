@@ -70,6 +70,7 @@ struct Handle {
   int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
   double* dev_scalars = nullptr;        // small device scratch (norms etc.)
   cudaEvent_t ev[8]{};   // 2,3: svd timing; 4,5: isometry fork/join; 6,7: iso solver debug
+  cudaEvent_t jev[2]{};  // ISO solver: the pending Jacobi launch (ms_jacobi)
   std::string last_error;
   int64_t kernel_count = 0;
   // per-call statistics
@@ -79,6 +80,9 @@ struct Handle {
   double min_gap = 1e300;
   int n_svd = 0;
   int n_svd_fallback = 0;               // CTM_SVD_ISO truncations handed to cuSOLVER
+  double ms_jacobi = 0.0;               // ISO solver: Jacobi launches, event-timed
+  double jacobi_flops = 0.0;
+  int n_jacobi = 0;
   int n_kernels = 0;
   bool dry = false;                     // sizing pass: no launches
   // CTM_FLAG_PROFILE: event pairs around each tc_gemm launch

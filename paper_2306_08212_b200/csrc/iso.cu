@@ -62,6 +62,9 @@ struct Solver {
   int last_sweeps = 0;
   int* repl;     // device: per-column "numerically dependent" flags (chol_kernel)
   unsigned seed = 0x9e3779b9u;
+  // event timing of the Jacobi launch pending since the last check_status (which syncs)
+  bool jac_pending = false;
+  int jac_n = 0, jac_max = 0, jac_slot = 0;
   explicit Solver(Handle& hh) : h(hh) {
     status = reinterpret_cast<int*>(h.ws.take(8));
     repl = reinterpret_cast<int*>(h.ws.take(LMAX_BIG / 2 + 1));
@@ -186,6 +189,7 @@ struct Solver {
     const size_t smem = (size_t)n * (n + 1) * sizeof(double);
     int* st = max_sweeps < 0 ? status + 1 : status + 4;   // capped runs report into a scratch slot
     const int ms = max_sweeps < 0 ? 60 : max_sweeps;
+    CTM_CUDA(cudaEventRecord(h.jev[0], h.stream));
     if (n > LMAX) {   // C5: 8-CTA cluster, rows split eight ways
       using J = JacCfg<8, 4, LMAX_BIG>;
       jacobi_cluster_kernel<8, 4, LMAX_BIG><<<8, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol);
@@ -200,6 +204,11 @@ struct Solver {
                                                                   max_sweeps < 0 ? 60 : max_sweeps, tol);
     }
     CTM_CUDA(cudaGetLastError());
+    CTM_CUDA(cudaEventRecord(h.jev[1], h.stream));
+    jac_pending = true;
+    jac_n = n;
+    jac_max = ms;
+    jac_slot = max_sweeps < 0 ? 2 : 5;   // status int index holding the sweep count
     h.count_kernel();
   }
   // Preconditioned one-sided Jacobi (Drmac & Veselic): the left singular vectors of
@@ -222,10 +231,20 @@ struct Solver {
   }
   void check_status(const char* what) {
     if (h.dry) return;
-    int st[3] = {0, 0, 0};
+    int st[6] = {0, 0, 0, 0, 0, 0};
     CTM_CUDA(cudaMemcpyAsync(st, status, sizeof(st), cudaMemcpyDeviceToHost, h.stream));
-    last_sweeps = st[2];
     CTM_CUDA(cudaStreamSynchronize(h.stream));
+    last_sweeps = st[2];
+    if (jac_pending) {
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.jev[0], h.jev[1]));
+      const int rep = st[jac_slot];
+      const int executed = rep < jac_max ? rep + 1 : jac_max;   // the kernel reports the index of its last sweep
+      h.ms_jacobi += ms;
+      h.jacobi_flops += 6.0 * jac_n * (double)jac_n * (jac_n - 1) * executed;
+      ++h.n_jacobi;
+      jac_pending = false;
+    }
     if (st[0] != 0) throw IsoFail(std::string(what) + ": CholQR pivot " + std::to_string(st[0]) + " not positive");
     if (st[1] != 0) throw IsoFail(std::string(what) + ": Jacobi did not converge");
   }
