@@ -316,7 +316,12 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     }
     if (debug_direct()) {
       sv.check_status("iso direct");
-      std::fprintf(stderr, "[iso] direct %d x %d keep %d: n=%d jacobi sweeps %d\n", R, C, n_keep, n, sv.last_sweeps);
+      std::vector<double> sd(n);
+      CTM_CUDA(cudaMemcpy(sd.data(), S, sizeof(double) * n, cudaMemcpyDeviceToHost));
+      int close = 0;
+      for (int i = 0; i + 1 < n; ++i) close += sd[i + 1] > 0.99 * sd[i];
+      std::fprintf(stderr, "[iso] direct %d x %d keep %d: n=%d jacobi sweeps %d  s: %.3g %.3g %.3g %.3g %.3g  pairs within 1%%: %d\n",
+                   R, C, n_keep, n, sv.last_sweeps, sd[0], sd[n / 4], sd[n / 2], sd[3 * n / 4], sd[n - 1], close);
     }
     const double* U = W;
     if (tall) {
