@@ -13,6 +13,7 @@
 #include <functional>
 #include <limits>
 #include <memory>
+#include <future>
 #include <thread>
 #include <exception>
 
@@ -352,44 +353,58 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
     ri[x] = RenvIn{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
   SideOut side[4];
   const bool reuse = cache != nullptr && cache->valid;
-  std::vector<std::function<void()>> A;
-  for (int i = 0; i < 4; ++i) {
-    if (reuse && (i % 2) == 1) {
-      side[i] = cache->side[i / 2];
-      continue;
-    }
-    A.push_back([&, i]() { side[i] = side_ts(*h.subs[i], ri[i / 2], (i % 2) == 0, p.chi_pp); });
-  }
-  run_parallel(h, A);
-  if (cache != nullptr && !cache->valid) {
-    for (int x = 0; x < 2; ++x) {
+  // Two independent chains, one per cut type x: [left side TS on sub 2x || right side TS on
+  // sub 2x+1] -> reduced env M_x + main TS on sub 2x.  Each chain waits only for its own
+  // right-side task (host future + stream event), not for the other chain's side tasks.
+  std::promise<void> right_done[2];
+  std::shared_future<void> right_fut[2] = {right_done[0].get_future().share(), right_done[1].get_future().share()};
+  auto right_task = [&](int x) {   // sub 2x+1: right side TS (+ its copy into the move's cache)
+    try {
       Handle& sub = *h.subs[2 * x + 1];
-      const SideOut& o = side[2 * x + 1];
-      Ten* dst[3] = {&cache->side[x].v.v1, &cache->side[x].v.v2, &cache->side[x].Q2};
-      const Ten* src[3] = {&o.v.v1, &o.v.v2, &o.Q2};
-      for (int t = 0; t < 3; ++t) {
-        if (dst[t]->size() != src[t]->size()) throw Error(CTM_E_ARG, "side cache: shape mismatch");
-        dst[t]->ext = src[t]->ext;
-        if (!h.dry)
-          CTM_CUDA(cudaMemcpyAsync(dst[t]->p, src[t]->p, src[t]->size() * 8, cudaMemcpyDeviceToDevice, sub.stream));
+      side[2 * x + 1] = side_ts(sub, ri[x], false, p.chi_pp);
+      if (cache != nullptr) {
+        const SideOut& o = side[2 * x + 1];
+        Ten* dst[3] = {&cache->side[x].v.v1, &cache->side[x].v.v2, &cache->side[x].Q2};
+        const Ten* src[3] = {&o.v.v1, &o.v.v2, &o.Q2};
+        for (int t = 0; t < 3; ++t) {
+          if (dst[t]->size() != src[t]->size()) throw Error(CTM_E_ARG, "side cache: shape mismatch");
+          dst[t]->ext = src[t]->ext;
+          if (!h.dry)
+            CTM_CUDA(cudaMemcpyAsync(dst[t]->p, src[t]->p, src[t]->size() * 8, cudaMemcpyDeviceToDevice, sub.stream));
+        }
       }
+      right_done[x].set_value();
+    } catch (...) {
+      right_done[x].set_exception(std::current_exception());
+      throw;
     }
-    cache->valid = true;
-  }
-  if (!h.dry)
-    for (int x = 0; x < 2; ++x) {   // phase B of x runs on sub 2x and needs sub 2x+1's outputs
-      Handle& r = *h.subs[2 * x + 1];
+  };
+  auto chain_task = [&](int x) {   // sub 2x: left side TS, then (after x's right side) a5
+    Handle& s = *h.subs[2 * x];
+    side[2 * x] = side_ts(s, ri[x], true, p.chi_pp);
+    if (reuse) side[2 * x + 1] = cache->side[x];
+    else right_fut[x].get();   // host: the right-side task has enqueued everything
+    Handle& r = *h.subs[2 * x + 1];
+    if (!h.dry) {   // device: sub 2x waits for sub 2x+1's stream (its outputs / the cached copy)
       CTM_CUDA(cudaEventRecord(r.ev[0], r.stream));
-      CTM_CUDA(cudaStreamWaitEvent(h.subs[2 * x]->stream, r.ev[0], 0));
+      CTM_CUDA(cudaStreamWaitEvent(s.stream, r.ev[0], 0));
     }
-  std::vector<std::function<void()>> B;
-  for (int x = 0; x < 2; ++x)
-    B.push_back([&, x]() {
-      Handle& s = *h.subs[2 * x];
-      RenvOut ro = renv_finish(s, ri[x], side[2 * x], side[2 * x + 1]);
-      V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr);   // a5
-    });
-  run_parallel(h, B);
+    RenvOut ro = renv_finish(s, ri[x], side[2 * x], side[2 * x + 1]);
+    V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr);   // a5
+  };
+  std::vector<std::function<void()>> T;
+  for (int x = 0; x < 2; ++x) {
+    T.push_back([&, x]() { chain_task(x); });
+    if (!reuse) T.push_back([&, x]() { right_task(x); });
+  }
+  if (h.dry) {   // sizing pass: sequential, right sides first (no waiting on futures)
+    if (!reuse)
+      for (int x = 0; x < 2; ++x) right_task(x);
+    for (int x = 0; x < 2; ++x) chain_task(x);
+  } else {
+    run_parallel(h, T);
+  }
+  if (cache != nullptr) cache->valid = true;
   for (auto& s : h.subs) {
     if (!h.dry) {
       CTM_CUDA(cudaEventRecord(s->ev[1], s->stream));   // join

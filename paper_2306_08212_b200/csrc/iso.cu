@@ -463,7 +463,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     const double rate = xk + std::sqrt(xk * xk - 1.0);
     // the first estimate comes from a young subspace (Ritz values of the block bottom are
     // low, the rate optimistic): over-filter by 1.6x rather than pay another check
-    const double safety = 1.25;   // (1.0 / 0.85 / 0.7 measured slower: an extra check)
+    const double safety = 1.25;   // (1.0 / 0.85 / 0.7 slower: an extra check; 1.6-2.5 on the flat G-form cuts: no change)
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
