@@ -173,7 +173,8 @@ struct Solver {
     for (int p = 0; p < passes; ++p) {
       const double sf = (shifted && p == 0) ? 11.0 * ((double)m * n + (double)n * (n + 1)) * EPS : 0.0;
       double* Rp = (Rtot && p == 0) ? Rtot : R;
-      cholqr_pass(Y, m, n, sf, Rp, replace && p == 1, passes == 1 ? also : nullptr);   // the first plain pass may replace columns
+      // the first plain pass may replace columns (a single pass: that pass, when not shifted)
+      cholqr_pass(Y, m, n, sf, Rp, replace && (p == 1 || (passes == 1 && !shifted)), passes == 1 ? also : nullptr);
       if (Rtot && p > 0) {   // Rtot <- R_p Rtot
         gemm(R, "ab", {n, n}, Rtot, "bc", {n, n}, T, "ac", {n, n});
         if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Rtot, T, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, h.stream));
@@ -473,7 +474,15 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // drown (seen as Ritz residual blow-ups at l = 288).
     const double shift_rel = 11.0 * ((double)R * l + (double)l * (l + 1)) * EPS;
     const double spread = std::min(1e6, 0.25 / std::sqrt(shift_rel));
-    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / (std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12))));
+    const double lg_deg = std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12;   // log-spread per degree
+    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / lg_deg)));
+    // Longer blocks re-orthonormalised by one PLAIN CholQR pass (no shift: kappa(Q) ~ 1, so
+    // nothing compounds) while the spread stays <= 1e7 (Gram condition 1e14 < 1/eps); the
+    // rounding noise such a block leaves in the kept directions (~ eps * spread) is filtered
+    // away by the last `tail` degrees, which use the short shifted blocks above.
+    static const int plain_on = std::getenv("CTM_ISO_PLAIN") ? std::atoi(std::getenv("CTM_ISO_PLAIN")) : 1;
+    const int mb_plain = std::max(1, std::min(12, (int)std::floor(std::log(1e7) / lg_deg)));
+    const int tail = 6;
     // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
     // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
     // (after the capped first check W is not orthogonal: keep filtering Y itself)
@@ -490,7 +499,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     double* bufs[2] = {Y1, Y2};
     int nb = 0, done = 0;
     while (done < need) {
-      const int m = std::min(mb, need - done);
+      const bool plain = plain_on && mb_plain > mb && need - done > tail;
+      const int m = plain ? std::min(mb_plain, need - done - tail) : std::min(mb, need - done);
       for (int j = 0; j < m; ++j) {
         GYf(Yc, P);
         double* Yn = bufs[nb];
@@ -505,7 +515,9 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
       }
-      sv.cholqr(Yc, R, l, 1, true, nullptr, false, Yo);
+      // (plain blocks replace numerically dependent columns instead of failing: the block's
+      // bottom columns -- the oversampling buffer -- can fall below eps of the top ones)
+      sv.cholqr(Yc, R, l, 1, !plain, nullptr, plain, Yo);
       done += m;
     }
     if (!h.dry && Yc != Y) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
