@@ -173,8 +173,8 @@ struct Solver {
     for (int p = 0; p < passes; ++p) {
       const double sf = (shifted && p == 0) ? 11.0 * ((double)m * n + (double)n * (n + 1)) * EPS : 0.0;
       double* Rp = (Rtot && p == 0) ? Rtot : R;
-      // the first plain pass may replace columns (a single pass: that pass, when not shifted)
-      cholqr_pass(Y, m, n, sf, Rp, replace && (p == 1 || (passes == 1 && !shifted)), passes == 1 ? also : nullptr);
+      // the first plain pass may replace numerically dependent columns
+      cholqr_pass(Y, m, n, sf, Rp, replace && p == (shifted ? 1 : 0), passes == 1 ? also : nullptr);
       if (Rtot && p > 0) {   // Rtot <- R_p Rtot
         gemm(R, "ab", {n, n}, Rtot, "bc", {n, n}, T, "ac", {n, n});
         if (!h.dry) CTM_CUDA(cudaMemcpyAsync(Rtot, T, sizeof(double) * n * n, cudaMemcpyDeviceToDevice, h.stream));
@@ -400,7 +400,12 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // Rayleigh-Ritz on an orthonormal Y: Z = M^T Y, P = M Z, Z = Q_z R_z, W = lsv(R_z^T)
     cudaEvent_t e_rr0 = h.ev[6], e_rr1 = h.ev[7];
     if (!h.dry && debug) CTM_CUDA(cudaEventRecord(e_rr0, h.stream));
-    sv.cholqr(Y, R, l, 3, true, nullptr, true);   // sCholQR3 (dependent columns replaced): orthonormal
+    // orthonormal basis: Y leaves the filter (or the start) through a shifted CholQR, so its
+    // condition is modest and plain CholQR2 suffices for l <= LMAX (the first pass replaces
+    // dependent columns; C4 64.8 -> 62.6 ms); at l > LMAX it cost C5 an extra check
+    // (260 -> 277 ms), which keeps shifted CholQR3 there
+    if (l <= LMAX) sv.cholqr(Y, R, l, 2, false, nullptr, true);
+    else sv.cholqr(Y, R, l, 3, true, nullptr, true);
     GY(Y, P);
     sv.cholqr(Z, C, l, 2, true, Rz);         // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR2)
     // the first Rayleigh-Ritz only seeds the filter bounds: a capped, loose Jacobi suffices
