@@ -326,7 +326,7 @@ def bench_ours(args, cfg):
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
         # the dominant kernel family of the step by device time (profiles/r01_final_ncu_launches_bench_step.txt:
-        # Jacobi 33%, Cholesky 28%, tc_gemm 23%): the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA
+        # Jacobi 32%, Cholesky 26%, tc_gemm 26%): the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA
         # cores, latency/issue-bound on 1-8 CTAs per launch; timed by CUDA events on the worker streams
         "roofline": ({"bound": "alu", "kernel": "jacobi_cluster_kernel (one-sided Jacobi, FP64 DFMA)",
                       "achieved": jac_achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
