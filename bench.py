@@ -300,6 +300,7 @@ def bench_ours(args, cfg):
     jac_fl = float(np.mean([s["jacobi_flops"] for s in stats]))
     jac_n = float(np.mean([s["n_jacobi"] for s in stats]))
     jac_achieved = jac_fl / (jac_ms * 1e-3) / 1e12 if jac_ms > 0 else None
+    jac_sms = float(np.mean([s["jacobi_cta_ms"] for s in stats])) / jac_ms if jac_ms > 0 else None
     if rank != 0:
         return
     value = job_value(world, t_step)
@@ -333,6 +334,8 @@ def bench_ours(args, cfg):
                       "frac": jac_achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
                       "launches_per_step": jac_n, "ms_per_step": jac_ms, "flops_per_step": jac_fl,
                       "flops_unit": "6 n^2 (n-1) per executed sweep",
+                      "sms_occupied_avg": jac_sms,
+                      "frac_of_occupied_sms": jac_achieved / (FP64_DFMA_PEAK_TFLOPS / 148 * jac_sms),
                       "peak_source": "measured DFMA loop, whole GPU (profiles/r01_probe_fp64.txt); one launch "
                                      "occupies 1-8 SMs, whose share of that peak is 1-8 x 0.25 TFLOP/s"}
                      if jac_achieved else None),

@@ -150,6 +150,7 @@ typedef struct {
   double ms_jacobi;     /* summed device time of the Jacobi launches                    */
   double jacobi_flops;  /* their algorithmic flops                                       */
   int n_jacobi;         /* number of Jacobi launches                                     */
+  double jacobi_cta_ms; /* sum of launch time x CTAs (one CTA per SM): SM-weighted time  */
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by

@@ -294,6 +294,7 @@ void sub_begin(Handle& s) {
   s.n_svd_fallback = 0;
   s.ms_jacobi = 0.0;
   s.jacobi_flops = 0.0;
+  s.jacobi_cta_ms = 0.0;
   s.n_jacobi = 0;
   s.n_kernels = 0;
   s.dry = false;
@@ -306,6 +307,7 @@ void sub_merge(Handle& h, Handle& s) {
   h.n_svd_fallback += s.n_svd_fallback;
   h.ms_jacobi += s.ms_jacobi;
   h.jacobi_flops += s.jacobi_flops;
+  h.jacobi_cta_ms += s.jacobi_cta_ms;
   h.n_jacobi += s.n_jacobi;
   h.n_kernels += s.n_kernels;
   h.kernel_count += s.n_kernels;
@@ -1092,6 +1094,7 @@ void begin_call(Handle& h) {
   h.n_svd_fallback = 0;
   h.ms_jacobi = 0.0;
   h.jacobi_flops = 0.0;
+  h.jacobi_cta_ms = 0.0;
   h.n_jacobi = 0;
   h.n_kernels = 0;
   h.prof_used = 0;
@@ -1112,6 +1115,7 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->ms_jacobi = h.ms_jacobi;
   st->jacobi_flops = h.jacobi_flops;
   st->n_jacobi = h.n_jacobi;
+  st->jacobi_cta_ms = h.jacobi_cta_ms;
   st->n_kernels = h.n_kernels;
   st->ms_gemm = 0.0;
   st->gemm_flops = 0.0;

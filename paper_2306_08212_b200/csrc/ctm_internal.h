@@ -82,6 +82,7 @@ struct Handle {
   int n_svd_fallback = 0;               // CTM_SVD_ISO truncations handed to cuSOLVER
   double ms_jacobi = 0.0;               // ISO solver: Jacobi launches, event-timed
   double jacobi_flops = 0.0;
+  double jacobi_cta_ms = 0.0;           // launch time x CTAs (1 CTA per SM): SM-weighted time
   int n_jacobi = 0;
   int n_kernels = 0;
   bool dry = false;                     // sizing pass: no launches

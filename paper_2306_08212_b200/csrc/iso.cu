@@ -64,7 +64,7 @@ struct Solver {
   unsigned seed = 0x9e3779b9u;
   // event timing of the Jacobi launch pending since the last check_status (which syncs)
   bool jac_pending = false;
-  int jac_n = 0, jac_max = 0, jac_slot = 0;
+  int jac_n = 0, jac_max = 0, jac_slot = 0, jac_ctas = 1;
   explicit Solver(Handle& hh) : h(hh) {
     status = reinterpret_cast<int*>(h.ws.take(8));
     repl = reinterpret_cast<int*>(h.ws.take(LMAX_BIG / 2 + 1));
@@ -210,6 +210,7 @@ struct Solver {
     jac_n = n;
     jac_max = ms;
     jac_slot = max_sweeps < 0 ? 2 : 5;   // status int index holding the sweep count
+    jac_ctas = n > LMAX ? 8 : (n > 128 ? 2 : 1);
     h.count_kernel();
   }
   // Preconditioned one-sided Jacobi (Drmac & Veselic): the left singular vectors of
@@ -242,6 +243,7 @@ struct Solver {
       const int rep = st[jac_slot];
       const int executed = rep < jac_max ? rep + 1 : jac_max;   // the kernel reports the index of its last sweep
       h.ms_jacobi += ms;
+      h.jacobi_cta_ms += ms * jac_ctas;
       h.jacobi_flops += 6.0 * jac_n * (double)jac_n * (jac_n - 1) * executed;
       ++h.n_jacobi;
       jac_pending = false;
@@ -459,7 +461,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // smallest Ritz value of the block), normalised at the k-th Ritz value; the error of
     // the slowest kept vector shrinks by x_k + sqrt(x_k^2 - 1) per degree.
     const double lk = s[k - 1] * s[k - 1], lb = s[l - 1] * s[l - 1], l1 = s[0] * s[0];
-    if (!have_G && l1 <= 16.0 * lk) {
+    if (!have_G && l1 <= 16.0 * lk) {   // (256 / 2500: within noise at C4/C5; not worth the floor)
       sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
       have_G = true;
     }

@@ -51,7 +51,7 @@ class ctm_move_stats(ctypes.Structure):
                 ("min_gap", c_double), ("n_svd", c_int), ("n_kernels", c_int), ("ms_gemm", c_double),
                 ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double),
                 ("n_svd_fallback", c_int), ("ms_jacobi", c_double), ("jacobi_flops", c_double),
-                ("n_jacobi", c_int)]
+                ("n_jacobi", c_int), ("jacobi_cta_ms", c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
