@@ -189,7 +189,10 @@ std::vector<int> chains(Handle& h, const std::vector<ChainJob>& jobs) {
 //   Q (P, D, D, F) as (boundary, ket, bra, far); returns v1 (P, D, n1), v2 (n1, D, n2) and
 //   optionally Q2 = v1^T Q (n1, D, F), which the reduced env reuses for C' (row a4).
 // ---------------------------------------------------------------------------------------
-Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep) {
+// side: the isometries only build the reduced environment M = C' T'^2 C'' (rows a3, a4),
+// where the stage-two output bond is contracted on both sides, so a non-truncating stage
+// two may return any orthonormal basis (reading R24): svd_left's basis_only.
+Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool side = false) {
   const int P = Qt.ext[0], K = Qt.ext[1], Bd = Qt.ext[2], F = Qt.ext[3];
   const int n1 = std::min(c1, P * K);
   Iso r;
@@ -199,7 +202,7 @@ Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep) {
   contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
   const int n2 = std::min(c2, n1 * Bd);
   r.v2 = alloc(h, {n1, Bd, n2});
-  svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p);
+  svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p, side);
   if (Q2_keep) *Q2_keep = Q2;
   return r;
 }
@@ -228,11 +231,11 @@ SideOut side_ts(Handle& h, const RenvIn& in, bool left, int chi_pp) {
   if (left) {   // Q_l(p,k,b,q) = sum_x C1(x,p) T1(q,k,b,x)
     Ten Q = alloc(h, {in.C1.ext[1], D, D, in.T1.ext[0]});
     contract(h, op({&in.C1}, "xp"), op({&in.T1}, "qkbx"), out({&Q}, "pkbq"));
-    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2);
+    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2, true);
   } else {      // Q_r(p,k,b,q) = sum_x C2(p,x) T3(x,k,b,q)
     Ten Q = alloc(h, {in.C2.ext[0], D, D, in.T3.ext[3]});
     contract(h, op({&in.C2}, "px"), op({&in.T3}, "xkbq"), out({&Q}, "pkbq"));
-    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2);
+    o.v = ts_isometry(h, Q, chi_pp, chi_pp, &o.Q2, true);
   }
   return o;
 }

@@ -125,11 +125,15 @@ void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* 
 // svd.cu: first n_keep left singular vectors of the row-major R x C matrix `mat`
 // (input preserved), written row-major (R, n_keep) with the sign rule.  Returns the
 // truncation gap sigma_{n}/sigma_{n+1} (inf if none).
-double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out);
+// basis_only: when nothing is truncated (n_keep == C <= R) and the caller's result does not
+// depend on the basis gauge, any orthonormal basis of the column space is returned
+// (CTM_SVD_ISO: shifted CholQR3, no SVD).
+double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out, bool basis_only = false);
 
 // iso.cu: libctm's own truncated SVD (subspace iteration + CholQR + one-sided Jacobi).
 #define CTM_ISO_LMAX 160
 void iso_init_kernels();
+void iso_basis(Handle& h, const double* mat, int R, int C, double* out);
 void singular_values(Handle& h, const double* mat, int R, int C, double* host_out);
 bool iso_supported(int R, int C, int n_keep);
 // ok = false when convergence could not be certified (caller falls back to cuSOLVER).

@@ -580,6 +580,20 @@ void singular_values(Handle& h, const double* mat, int R, int C, double* host_ou
   h.ws.reset(mark);
 }
 
+// An orthonormal basis of the column space of a tall R x C matrix (R >= C), written
+// row-major (R, C) into `out`: shifted CholQR3 of a copy (dependent columns replaced by
+// random directions, so the basis is complete even for a rank-deficient matrix).  For a
+// non-truncating cut whose basis gauge cancels downstream (svd_left's basis_only).
+void iso_basis(Handle& h, const double* mat, int R, int C, double* out) {
+  const size_t mark = h.ws.top;
+  Solver sv(h);
+  if (!h.dry) CTM_CUDA(cudaMemcpyAsync(out, mat, sizeof(double) * R * C, cudaMemcpyDeviceToDevice, h.stream));
+  sv.cholqr(out, R, C, 3, true, nullptr, true);
+  ++h.n_svd;
+  sv.check_status("iso basis");
+  h.ws.reset(mark);
+}
+
 double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
                         void (*signfix)(Handle&, const double*, long long, long long, int, int, double*), bool* ok) {
   *ok = true;

@@ -198,8 +198,20 @@ double svd_left_gram(Handle& h, const double* mat, int R, int C, int n_keep, dou
 
 }  // namespace
 
-double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out) {
+double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out, bool basis_only) {
   if (n_keep < 1 || n_keep > R) throw Error(CTM_E_ARG, "svd_left: n_keep out of range");
+  if (basis_only && h.prm.svd_algo == CTM_SVD_ISO && n_keep == C && C <= R) {
+    if (!h.dry) CTM_CUDA(cudaEventRecord(h.ev[2], h.stream));
+    iso_basis(h, mat, R, C, out);   // synchronises the stream
+    if (!h.dry) {
+      CTM_CUDA(cudaEventRecord(h.ev[3], h.stream));
+      CTM_CUDA(cudaEventSynchronize(h.ev[3]));
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[2], h.ev[3]));
+      h.ms_svd += ms;
+    }
+    return std::numeric_limits<double>::infinity();
+  }
   if (use_gram(h, R, C, n_keep)) return svd_left_gram(h, mat, R, C, n_keep, out);
   if (h.prm.svd_algo == CTM_SVD_ISO && iso_supported(R, C, n_keep)) {
     if (!h.dry) CTM_CUDA(cudaEventRecord(h.ev[2], h.stream));
