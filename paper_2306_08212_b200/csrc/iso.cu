@@ -172,7 +172,8 @@ struct Solver {
     double* T = Rtot ? h.ws.take((size_t)n * n) : nullptr;
     for (int p = 0; p < passes; ++p) {
       const double sf = (shifted && p == 0) ? 11.0 * ((double)m * n + (double)n * (n + 1)) * EPS : 0.0;
-      double* Rp = (Rtot && p == 0) ? Rtot : R;
+      // the dense R is needed only to accumulate Rtot, or by the two-block path (l > LMAX)
+      double* Rp = (Rtot && p == 0) ? Rtot : ((Rtot || n > LMAX) ? R : nullptr);
       // the first plain pass may replace numerically dependent columns
       cholqr_pass(Y, m, n, sf, Rp, replace && p == (shifted ? 1 : 0), passes == 1 ? also : nullptr);
       if (Rtot && p > 0) {   // Rtot <- R_p Rtot
