@@ -252,10 +252,14 @@ def bench_ours(args, cfg):
             e1.synchronize()
             ms_g.append(e0.elapsed_time(e1))
         del graph
-        # per-launch profile of the dominant kernel (tc_gemm), same contraction-only step
+        # per-launch profile of tc_gemm: the contraction-only step, and the full step (the
+        # isometry solvers' GEMMs on the worker streams included)
         pst = []
         for _ in range(3):
             step(inject=True, handle=hp, stats=pst)
+        pfull = []
+        for _ in range(3):
+            step(inject=False, handle=hp, stats=pfull)
         # end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
         pinned = {"A": torch.from_numpy(g["A"]).pin_memory(), "B": torch.from_numpy(g["B"]).pin_memory()}
         hC = {k: torch.from_numpy(v.reshape(-1)).pin_memory() for k, v in g["C"].items()}
@@ -296,6 +300,10 @@ def bench_ours(args, cfg):
     gem_fl = float(np.mean([s["gemm_flops"] for s in pst]))
     gem_n = float(np.mean([s["gemm_launches"] for s in pst]))
     achieved = gem_fl / (gem_ms * 1e-3) / 1e12
+    full_ms = float(np.mean([s["ms_gemm"] for s in pfull]))
+    full_fl = float(np.mean([s["gemm_flops"] for s in pfull]))
+    full_n = float(np.mean([s["gemm_launches"] for s in pfull]))
+    full_achieved = full_fl / (full_ms * 1e-3) / 1e12
     jac_ms = float(np.mean([s["ms_jacobi"] for s in stats]))
     jac_fl = float(np.mean([s["jacobi_flops"] for s in stats]))
     jac_n = float(np.mean([s["n_jacobi"] for s in stats]))
@@ -327,9 +335,18 @@ def bench_ours(args, cfg):
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
         # the dominant kernel family of the step by device time (profiles/r01_final_ncu_launches_bench_step.txt:
-        # Jacobi 32%, Cholesky 26%, tc_gemm 26%): the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA
-        # cores, latency/issue-bound on 1-8 CTAs per launch; timed by CUDA events on the worker streams
-        "roofline": ({"bound": "alu", "kernel": "jacobi_cluster_kernel (one-sided Jacobi, FP64 DFMA)",
+        # tc_gemm 30%, Cholesky 27%, Jacobi 24%): tc_gemm over every launch of the full step -- the absorption's
+        # contraction chains and the isometry solvers' small GEMMs -- timed by CUDA events on each launch's stream
+        "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4), all launches of the full step",
+                     "achieved": full_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": full_achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "launches_per_step": full_n, "ms_per_step": full_ms, "flops_per_step": full_fl,
+                     "note": "the solver GEMMs are 1024 x 160-class, latency bound (split-K); the contraction "
+                             "launches alone: roofline_contraction",
+                     "peak_source": "measured DMMA loop (profiles/r01_probe_fp64.txt); MEASURED_PEAKS.json has no FP64"},
+        # the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA cores, latency/issue-bound on 1-8 CTAs
+        # per launch; timed by CUDA events on the worker streams
+        "roofline_jacobi": ({"bound": "alu", "kernel": "jacobi_cluster_kernel (one-sided Jacobi, FP64 DFMA)",
                       "achieved": jac_achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                       "frac": jac_achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
                       "launches_per_step": jac_n, "ms_per_step": jac_ms, "flops_per_step": jac_fl,

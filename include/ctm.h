@@ -137,7 +137,8 @@ typedef struct {
   double min_gap;       /* min sigma_n / sigma_{n+1} over every truncation of the call  */
   int n_svd;            /* SVDs run                                                    */
   int n_kernels;        /* libctm kernels launched (excluding cuSOLVER internals)       */
-  /* CTM_FLAG_PROFILE only: the contraction kernel (tc_gemm) timed launch by launch */
+  /* CTM_FLAG_PROFILE only: the contraction kernel (tc_gemm) timed launch by launch, on the
+     caller's stream and on the isometry workers' streams (their solver GEMMs included) */
   double ms_gemm;       /* summed device time of the tc_gemm launches                  */
   double gemm_flops;    /* their algorithmic flops (sum of 2 M N K)                     */
   int gemm_launches;    /* number of tc_gemm launches                                  */

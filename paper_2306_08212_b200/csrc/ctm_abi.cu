@@ -313,6 +313,17 @@ void sub_merge(Handle& h, Handle& s) {
   h.jacobi_cta_ms += s.jacobi_cta_ms;
   h.n_jacobi += s.n_jacobi;
   h.n_kernels += s.n_kernels;
+  if (s.prof_used && !h.dry) {   // CTM_FLAG_PROFILE: the workers' tc_gemm launches (blocks the host)
+    CTM_CUDA(cudaEventSynchronize(s.prof_ev[2 * s.prof_used - 1]));
+    for (int i = 0; i < s.prof_used; ++i) {
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, s.prof_ev[2 * i], s.prof_ev[2 * i + 1]));
+      h.prof_ms_subs += ms;
+      h.prof_flops_subs += s.prof_flops[i];
+    }
+    h.prof_n_subs += s.prof_used;
+  }
+  s.prof_used = 0;
   h.kernel_count += s.n_kernels;
 }
 
@@ -1101,6 +1112,9 @@ void begin_call(Handle& h) {
   h.n_jacobi = 0;
   h.n_kernels = 0;
   h.prof_used = 0;
+  h.prof_ms_subs = 0.0;
+  h.prof_flops_subs = 0.0;
+  h.prof_n_subs = 0;
   if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
   h.ws.reset(0);
 }
@@ -1120,9 +1134,9 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->n_jacobi = h.n_jacobi;
   st->jacobi_cta_ms = h.jacobi_cta_ms;
   st->n_kernels = h.n_kernels;
-  st->ms_gemm = 0.0;
-  st->gemm_flops = 0.0;
-  st->gemm_launches = h.prof_used;
+  st->ms_gemm = h.prof_ms_subs;
+  st->gemm_flops = h.prof_flops_subs;
+  st->gemm_launches = h.prof_used + h.prof_n_subs;
   if (h.prof_used) {
     CTM_CUDA(cudaEventSynchronize(h.prof_ev[2 * h.prof_used - 1]));
     for (int i = 0; i < h.prof_used; ++i) {
@@ -1268,8 +1282,7 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
     init_solver(h, &h.prm);
     for (int i = 0; i < 4; ++i) {   // workers of the isometry stage (4 side TS, 2 main TS)
       std::unique_ptr<Handle> s(new Handle());
-      s->prm = h.prm;
-      s->prm.flags &= ~CTM_FLAG_PROFILE;
+      s->prm = h.prm;   // (CTM_FLAG_PROFILE kept: the solver's GEMMs are timed too)
       CTM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
       s->owns_stream = true;
       init_solver(*s, &s->prm);

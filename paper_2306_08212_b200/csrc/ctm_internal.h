@@ -90,6 +90,8 @@ struct Handle {
   std::vector<cudaEvent_t> prof_ev;
   std::vector<double> prof_flops;
   int prof_used = 0;
+  double prof_ms_subs = 0.0, prof_flops_subs = 0.0;   // worker sub-handles' launches, merged
+  int prof_n_subs = 0;
   // worker sub-handles (own stream + cuSOLVER handle + workspace slice) for the
   // independent isometry tasks of a column absorption; cuSOLVER blocks the calling host
   // thread, so each worker is driven by its own host thread.
