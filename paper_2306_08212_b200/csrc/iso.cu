@@ -481,6 +481,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // 1.25 (1.0 / 0.85 / 0.7: an extra check); 2.0 for the first plan of a flat (G-form) cut,
     // whose cheap degrees (one GEMM each) buy back a check: flat C4 solves 14 -> 12.3 ms, the
     // move 56.6 -> 53.6 ms (3.0 over-filters; at l > LMAX -- C5 -- it measured 2-3% slower)
+    // (1.6 / 2.5, or also for the second plan: within noise)
     const double safety = (checks == 1 && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? 2.0 : 1.25;
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
