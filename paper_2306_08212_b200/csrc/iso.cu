@@ -107,8 +107,12 @@ struct Solver {
     } else {
       chol_two_block(S, n, shift_factor, R, rd, replace);
     }
-    trsm(Y, m, n, R, rd, Rpk, nullptr);
-    if (also) trsm(also, m, n, R, rd, Rpk, nullptr);
+    if (n <= LMAX) {
+      trsm(Y, m, n, R, rd, Rpk, nullptr, also);   // (both matrices in one launch)
+    } else {
+      trsm(Y, m, n, R, rd, Rpk, nullptr);
+      if (also) trsm(also, m, n, R, rd, Rpk, nullptr);
+    }
     if (replace) {
       replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
       CTM_CUDA(cudaGetLastError());
@@ -116,12 +120,17 @@ struct Solver {
     }
     h.ws.reset(mark);
   }
-  void trsm(double* Y, int m, int n, const double* R, const double* rd, const double* Rpk, const int* dep) {
+  void trsm(double* Y, int m, int n, const double* R, const double* rd, const double* Rpk, const int* dep,
+            double* Y2 = nullptr) {
     const int rows_per_cta = 8;
-    const int grid = std::max(1, std::min(4 * 148, (m + rows_per_cta - 1) / rows_per_cta));
+    const int rows = Y2 ? 2 * m : m;
+    const int grid = std::max(1, std::min(4 * 148, (rows + rows_per_cta - 1) / rows_per_cta));
+    // one CTA per SM holds the 144 KB operand: 16 warps when the rows exceed 148 x 8
+    const int threads = rows > 148 * 8 ? 512 : 256;
+    const int grid_s = std::max(1, std::min(148, (rows + threads / 32 - 1) / (threads / 32)));
     if (n <= LMAX)
-      trsm_rows_kernel<(LMAX + 31) / 32><<<std::min(grid, 148), 256, rpk_size(n) * sizeof(double), h.stream>>>(
-          Y, m, n, Rpk, dep);
+      trsm_rows_kernel<(LMAX + 31) / 32><<<grid_s, threads, rpk_size(n) * sizeof(double), h.stream>>>(
+          Y, m, n, Rpk, dep, Y2);
     else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
