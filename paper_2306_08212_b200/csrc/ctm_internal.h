@@ -1,5 +1,7 @@
 // ctm_internal.h -- host-side internals of libctm (not part of the ABI).
 #pragma once
+#include <cstdlib>
+#include <utility>
 #include <cuda_runtime.h>
 #include <cusolverDn.h>
 
@@ -142,5 +144,28 @@ bool iso_supported(int R, int C, int n_keep);
 double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, double* out,
                         void (*signfix)(Handle&, const double*, long long, long long, int, int, double*), bool* ok);
 size_t svd_workspace_doubles(Handle& h, int R, int C);
+
+
+// Kernel launch with programmatic dependent launch (pdl.cuh) unless CTM_NO_PDL is set: the
+// kernel must call CTM_PDL_WAIT() before touching global memory.
+inline bool pdl_enabled() {
+  static const bool on = std::getenv("CTM_NO_PDL") == nullptr;
+  return on;
+}
+template <typename... KArgs, typename... Args>
+void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  const bool pdl = pdl_enabled();
+  cfg.attrs = pdl ? at : nullptr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  CTM_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
+}
 
 }  // namespace ctm

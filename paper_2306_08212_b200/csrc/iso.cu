@@ -100,8 +100,8 @@ struct Solver {
       return;
     }
     if (n <= LMAX) {
-      chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n), h.stream>>>(S, n, shift_factor, R, rd, status, replace ? 1e-13 : 0.0,
-                                                            replace ? repl : nullptr, nullptr, Rpk);
+      launch_k(chol_kernel, dim3(1), dim3(CHOL_THREADS), chol_smem_bytes(n), h.stream, (const double*)S, n, shift_factor,
+               R, rd, status, replace ? 1e-13 : 0.0, replace ? repl : nullptr, (const double*)nullptr, Rpk);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
     } else {
@@ -129,8 +129,8 @@ struct Solver {
     const int threads = rows > 148 * 8 ? 512 : 256;
     const int grid_s = std::max(1, std::min(148, (rows + threads / 32 - 1) / (threads / 32)));
     if (n <= LMAX)
-      trsm_rows_kernel<(LMAX + 31) / 32><<<grid_s, threads, rpk_size(n) * sizeof(double), h.stream>>>(
-          Y, m, n, Rpk, dep, Y2);
+      launch_k(trsm_rows_kernel<(LMAX + 31) / 32>, dim3(grid_s), dim3(threads), rpk_size(n) * sizeof(double), h.stream,
+               Y, m, n, Rpk, dep, Y2);
     else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
@@ -204,13 +204,16 @@ struct Solver {
     CTM_CUDA(cudaEventRecord(h.jev[0], h.stream));
     if (n > LMAX) {   // C5: 8-CTA cluster, rows split eight ways
       using J = JacCfg<8, 4, LMAX_BIG>;
-      jacobi_cluster_kernel<8, 4, LMAX_BIG><<<8, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol, skip_tol);
+      launch_k(jacobi_cluster_kernel<8, 4, LMAX_BIG>, dim3(8), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S,
+               st, ms, tol, skip_tol);
     } else if (n > 128) {   // register-resident 2-CTA cluster: 1.4x faster per sweep at l = 160
       using J = JacCfg<2, 8, LMAX>;
-      jacobi_cluster_kernel<2, 8, LMAX><<<2, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol, skip_tol);
+      launch_k(jacobi_cluster_kernel<2, 8, LMAX>, dim3(2), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S, st,
+               ms, tol, skip_tol);
     } else if (n > 32 && !std::getenv("CTM_ISO_JAC_SMEM")) {   // register-resident, one CTA
       using J = JacCfg<1, 8, 128>;
-      jacobi_cluster_kernel<1, 8, 128><<<1, J::THREADS, J::SMEM, h.stream>>>(X, n, trans, ncols, U, S, st, ms, tol, skip_tol);
+      launch_k(jacobi_cluster_kernel<1, 8, 128>, dim3(1), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S, st,
+               ms, tol, skip_tol);
     } else {
       jacobi_lsv_kernel<<<1, jacobi_threads(n), smem, h.stream>>>(X, n, trans, ncols, U, S, st,
                                                                   max_sweeps < 0 ? 60 : max_sweeps, tol);
@@ -387,7 +390,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   };
   auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c) {
     if (h.dry) return;
-    cheb_combine_kernel<<<148, 256, 0, h.stream>>>(out, Pm, Yc, Yo, (long long)R * l, a, b2, c);
+    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, Pm, Yc, Yo, (long long)R * l, a, b2, c);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   };

@@ -12,6 +12,7 @@ namespace {
 
 // Split-K reduction: C[off(m,n)] = alpha * sum_s P[b][s][m][n] (+ beta C), in split order.
 __global__ void splitk_reduce_kernel(const TcArgs args) {
+  CTM_PDL_WAIT();
   const int b = blockIdx.y;
   const long long MN = (long long)args.M * args.N;
   double ss = 0.0;
@@ -91,7 +92,7 @@ void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
     attr_set = true;
   }
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
-  kern<<<grid, C_::THREADS, C_::SMEM_BYTES, h.stream>>>(a);
+  launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
@@ -323,7 +324,7 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     prof_begin();
     launch_idx(h, best, a, batch * best_splits);
     int rb = (int)std::min<long long>(2 * kSMs, ((long long)M * N + 255) / 256);
-    splitk_reduce_kernel<<<dim3(rb, batch), 256, 0, h.stream>>>(a);
+    launch_k(splitk_reduce_kernel, dim3(rb, batch), dim3(256), 0, h.stream, a);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
     prof_end(2.0 * (double)M * N * K * batch);

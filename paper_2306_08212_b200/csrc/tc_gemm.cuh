@@ -28,6 +28,7 @@
 //    sums them in split order (no floating-point atomics on the data).
 //  * batch: one launch serves up to CTM_MAXBATCH problems with identical shapes/strides.
 #pragma once
+#include "pdl.cuh"
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -189,6 +190,9 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   for (int k = tid; k < kcount; k += THREADS)
     mode_offset2(kbase + k, args.nk, args.k_ext, args.k_mag, args.k_sh, args.a_k, args.b_k, a_koff[k], b_koff[k]);
   __syncthreads();
+  // programmatic dependent launch: the offset tables above use only the arguments, so they
+  // overlap the previous kernel's tail; operands are read after the wait
+  CTM_PDL_WAIT();
 
   // ---- per-thread load assignment (fixed across stages) -----------------------------
   // A: k-fast -> fixed kl, rows ml0 + j*(THREADS/BK);  m-fast -> fixed ml, kl0 + j*(THREADS/BM)
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
     cp_async_commit();
   }
   cp_async_wait<0>();
+  CTM_PDL_TRIGGER();
 
   // ---- epilogue: direct stores from the accumulator layout ---------------------------
   const double alpha = args.alpha, beta = args.beta;
