@@ -114,7 +114,7 @@ struct Solver {
       if (also) trsm(also, m, n, R, rd, Rpk, nullptr);
     }
     if (replace) {
-      replace_cols_kernel<<<std::min(n, 148), 256, 0, h.stream>>>(Y, m, n, repl, seed += 0x6a09e667u);
+      launch_k(replace_cols_kernel, dim3(std::min(n, 148)), dim3(256), 0, h.stream, Y, m, n, repl, seed += 0x6a09e667u);
       CTM_CUDA(cudaGetLastError());
       h.count_kernel();
     }
@@ -131,7 +131,7 @@ struct Solver {
     if (n <= LMAX)
       launch_k(trsm_rows_kernel<(LMAX + 31) / 32>, dim3(grid_s), dim3(threads), rpk_size(n) * sizeof(double), h.stream,
                Y, m, n, Rpk, dep, Y2);
-    else trsm_rows_big_kernel<<<grid, 256, 0, h.stream>>>(Y, m, n, R, rd);   // dep: only used at n1 = LMAX
+    else launch_k(trsm_rows_big_kernel, dim3(grid), dim3(256), 0, h.stream, Y, m, n, R, rd);   // dep: only at n1 = LMAX
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   }
@@ -152,7 +152,7 @@ struct Solver {
       return;
     }
     const double tol = replace ? 1e-13 : 0.0;
-    chol_diag_shift_kernel<<<1, 256, 0, h.stream>>>(S, n, shift_factor, dref);
+    launch_k(chol_diag_shift_kernel, dim3(1), dim3(256), 0, h.stream, S, n, shift_factor, dref);
     CTM_CUDA(cudaGetLastError());
     const size_t sz = sizeof(double);
     CTM_CUDA(cudaMemcpy2DAsync(S11, n1 * sz, S, n * sz, n1 * sz, n1, cudaMemcpyDeviceToDevice, h.stream));
@@ -163,12 +163,13 @@ struct Solver {
                                                          dref, Rpk1);
     CTM_CUDA(cudaGetLastError());
     trsm(W, n2, n1, R11, rd, Rpk1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
-    chol_schur_kernel<<<dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream>>>(S22, W, n2, n1);
+    launch_k(chol_schur_kernel, dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream, S22, (const double*)W, n2, n1);
     CTM_CUDA(cudaGetLastError());
     chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n2), h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
                                                          replace ? repl + n1 : nullptr, dref + n1);
     CTM_CUDA(cudaGetLastError());
-    chol_assemble_kernel<<<std::min(148, (n * n + 255) / 256), 256, 0, h.stream>>>(R, n, n1, R11, W, R22);
+    launch_k(chol_assemble_kernel, dim3(std::min(148, (n * n + 255) / 256)), dim3(256), 0, h.stream, R, n, n1,
+             (const double*)R11, (const double*)W, (const double*)R22);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel(5);
     h.ws.reset(mark);
@@ -442,7 +443,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       h.ws.reset(mark);
       return inf;
     }
-    ritz_residual_kernel<<<k, 256, 0, h.stream>>>(PW, U, S, R, l, k, res);
+    launch_k(ritz_residual_kernel, dim3(k), dim3(256), 0, h.stream, (const double*)PW, (const double*)U, (const double*)S,
+             R, l, k, res);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
     if (debug) CTM_CUDA(cudaEventRecord(e_rr1, h.stream));
