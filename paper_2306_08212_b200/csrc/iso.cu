@@ -159,14 +159,14 @@ struct Solver {
     CTM_CUDA(cudaMemcpy2DAsync(W, n1 * sz, S + (size_t)n1 * n, n * sz, n1 * sz, n2, cudaMemcpyDeviceToDevice, h.stream));
     CTM_CUDA(cudaMemcpy2DAsync(S22, n2 * sz, S + (size_t)n1 * n + n1, n * sz, n2 * sz, n2, cudaMemcpyDeviceToDevice,
                                h.stream));
-    chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n1), h.stream>>>(S11, n1, 0.0, R11, rd, status, tol, replace ? repl : nullptr,
-                                                         dref, Rpk1);
+    launch_k(chol_kernel, dim3(1), dim3(CHOL_THREADS), chol_smem_bytes(n1), h.stream, (const double*)S11, n1, 0.0, R11,
+             rd, status, tol, replace ? repl : nullptr, (const double*)dref, Rpk1);
     CTM_CUDA(cudaGetLastError());
     trsm(W, n2, n1, R11, rd, Rpk1, replace ? repl : nullptr);   // W = S21 R11^{-1} = R12^T
     launch_k(chol_schur_kernel, dim3((n2 + 15) / 16, (n2 + 15) / 16), dim3(16, 16), 0, h.stream, S22, (const double*)W, n2, n1);
     CTM_CUDA(cudaGetLastError());
-    chol_kernel<<<1, CHOL_THREADS, chol_smem_bytes(n2), h.stream>>>(S22, n2, 0.0, R22, rd + n1, status, tol,
-                                                         replace ? repl + n1 : nullptr, dref + n1);
+    launch_k(chol_kernel, dim3(1), dim3(CHOL_THREADS), chol_smem_bytes(n2), h.stream, (const double*)S22, n2, 0.0, R22,
+             rd + n1, status, tol, replace ? repl + n1 : nullptr, (const double*)(dref + n1), (double*)nullptr);
     CTM_CUDA(cudaGetLastError());
     launch_k(chol_assemble_kernel, dim3(std::min(148, (n * n + 255) / 256)), dim3(256), 0, h.stream, R, n, n1,
              (const double*)R11, (const double*)W, (const double*)R22);
@@ -397,7 +397,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   };
   // start: Y = orth(M Omega), then two plain steps Y <- orth(M M^T Y)
   if (!h.dry) {
-    fill_omega_kernel<<<148, 256, 0, h.stream>>>(Z, (long long)C * l, 0x5eed1234u);
+    launch_k(fill_omega_kernel, dim3(148), dim3(256), 0, h.stream, Z, (long long)C * l, 0x5eed1234u);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   }

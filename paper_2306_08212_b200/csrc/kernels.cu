@@ -2,6 +2,7 @@
 // norms (sum of squares), normalise-and-commit, finiteness scan.  Grid sizes are
 // multiples of the 148 SMs (grid-stride loops).
 #include "ctm_internal.h"
+#include "pdl.cuh"
 
 namespace ctm {
 namespace {
@@ -16,6 +17,7 @@ struct PermArgs {
 
 __global__ void permute_kernel(const double* __restrict__ src, double* __restrict__ dst, long long n,
                                PermArgs a) {
+  CTM_PDL_WAIT();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     long long r = i, off = 0;
@@ -46,6 +48,7 @@ struct Multi {
 
 // blockIdx.y = tensor; out[y] += sum of squares
 __global__ void sumsq_kernel(Multi m, double* out) {
+  CTM_PDL_WAIT();
   const int y = blockIdx.y;
   const double* __restrict__ s = m.src[y];
   const long long n = m.n[y];
@@ -69,6 +72,7 @@ __global__ void sumsq_kernel(Multi m, double* out) {
 // dst[y][i] = src[y][i] / ||src[y]||_F   (Frobenius normalisation, reading R13); the norm
 // is the in-order sum of the per-tile partials written by the producing GEMM (deterministic).
 __global__ void scale_commit_kernel(Multi m, const double* __restrict__ ss, Parts parts) {
+  CTM_PDL_WAIT();
   const int y = blockIdx.y;
   __shared__ double inv_s;
   if (threadIdx.x == 0) {
@@ -185,7 +189,7 @@ void permute(Handle& h, const double* src, const std::vector<int>& ext, const st
     a.dst_ext[j] = ext[perm[j]];
     a.src_str[j] = st[perm[j]];
   }
-  permute_kernel<<<grid_for(acc), 256, 0, h.stream>>>(src, dst, acc, a);
+  launch_k(permute_kernel, dim3(grid_for(acc)), dim3(256), 0, h.stream, src, dst, acc, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
@@ -208,7 +212,7 @@ void sumsq(Handle& h, const std::vector<const double*>& srcs, const std::vector<
     mx = std::max(mx, m.n[i]);
   }
   dim3 grid(std::min(grid_for(mx), kSMs * 2), (unsigned)srcs.size());
-  sumsq_kernel<<<grid, 256, 0, h.stream>>>(m, out);
+  launch_k(sumsq_kernel, dim3(grid), dim3(256), 0, h.stream, m, out);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
@@ -227,7 +231,7 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
     mx = std::max(mx, m.n[i]);
   }
   dim3 grid(std::min(grid_for(mx), kSMs * 2), (unsigned)srcs.size());
-  scale_commit_kernel<<<grid, 256, 0, h.stream>>>(m, ss, parts);
+  launch_k(scale_commit_kernel, dim3(grid), dim3(256), 0, h.stream, m, (const double*)ss, parts);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }

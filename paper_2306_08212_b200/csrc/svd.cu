@@ -9,6 +9,7 @@
 #include <limits>
 
 #include "ctm_internal.h"
+#include "pdl.cuh"
 
 namespace ctm {
 namespace {
@@ -23,6 +24,7 @@ namespace {
 // One block per kept column j: x_i = base[i*rs + j*cs], i < R.
 __global__ void extract_signfix_kernel(const double* __restrict__ base, long long rs, long long cs, int R,
                                        int n_keep, double* __restrict__ out) {
+  CTM_PDL_WAIT();
   const int j = blockIdx.x;
   const double* col = base + j * cs;
   double best = -1.0;
@@ -126,7 +128,7 @@ size_t query_lwork_bytes(Handle& h, const Plan& p, double* A, double* S, double*
 }
 
 void signfix_launch(Handle& h, const double* base, long long rs, long long cs, int R, int n_keep, double* out) {
-  extract_signfix_kernel<<<n_keep, 256, 0, h.stream>>>(base, rs, cs, R, n_keep, out);
+  launch_k(extract_signfix_kernel, dim3(n_keep), dim3(256), 0, h.stream, base, rs, cs, R, n_keep, out);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
@@ -283,7 +285,7 @@ double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* 
       break;
     }
   }
-  extract_signfix_kernel<<<n_keep, 256, 0, h.stream>>>(vecs, rs, cs, R, n_keep, out);
+  launch_k(extract_signfix_kernel, dim3(n_keep), dim3(256), 0, h.stream, (const double*)vecs, rs, cs, R, n_keep, out);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
   CTM_CUDA(cudaEventRecord(h.ev[3], h.stream));
