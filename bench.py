@@ -335,7 +335,7 @@ def bench_ours(args, cfg):
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
         # the dominant kernel family of the step by device time (profiles/r01_final_ncu_launches_bench_step.txt:
-        # tc_gemm 33%, Cholesky 27%, Jacobi 25%): tc_gemm over every launch of the full step -- the absorption's
+        # tc_gemm 34%, Jacobi 26%, Cholesky 25%): tc_gemm over every launch of the full step -- the absorption's
         # contraction chains and the isometry solvers' small GEMMs -- timed by CUDA events on each launch's stream
         "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4), all launches of the full step",
                      "achieved": full_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
