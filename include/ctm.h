@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CTM_ABI_VERSION 1
+#define CTM_ABI_VERSION 2
 
 /* status codes */
 #define CTM_OK 0
@@ -152,6 +152,14 @@ typedef struct {
   double jacobi_flops;  /* their algorithmic flops                                       */
   int n_jacobi;         /* number of Jacobi launches                                     */
   double jacobi_cta_ms; /* sum of launch time x CTAs (one CTA per SM): SM-weighted time  */
+  /* Per-cut truncation gaps sigma_n / sigma_{n+1} of the stage-one SVD (SURVEY 8(b),
+     8(d) "log min sigma_chi/sigma_{chi+1} per cut"), the minimum over the moves of the call;
+     +inf where nothing was truncated or the isometries were injected.
+       cut_gap[a][c]:  main TS(M; chi', chi) of absorption a = 0, 1, cut c = ab (0), ba (1);
+       side_gap[a][i]: side TS(Q; chi'', chi'') of absorption a, i = a-left, a-right,
+                       b-left, b-right (Q_l = C^1 T^1, Q_r = C^2 T^3).             */
+  double cut_gap[2][2];
+  double side_gap[2][4];
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by
@@ -240,9 +248,9 @@ int ctm_norm_2x2(ctm_handle h, const double* A, const double* B, const ctm_env* 
  * e_out_host: the energy.  Synchronises the stream. */
 /* ctm_site_spins: single-site spin expectations for d = 2 (S = sigma/2), from the H-bond
  * 2x1-window rho by partial trace ("staggered magnetization"; DESIGN.md
- * reading R23).  out_host[4] = <S^x>_A, <S^z>_A, <S^x>_B, <S^z>_B (<S^y> = 0 for real
- * tensors); the staggered magnetisation is m_s = (|<S>_A| + |<S>_B|) / 2.  Synchronises
- * the stream.  d != 2: CTM_E_UNSUPPORTED. */
+ * reading R23).  out_host[5] = <S^x>_A, <S^z>_A, <S^x>_B, <S^z>_B (<S^y> = 0 for real
+ * tensors) and the staggered magnetisation m_s = (|<S>_A| + |<S>_B|) / 2, all computed on
+ * the device.  Synchronises the stream.  d != 2: CTM_E_UNSUPPORTED. */
 int ctm_site_spins(ctm_handle h, const double* A, const double* B, const ctm_env* env, double* out_host);
 
 int ctm_bond_energy(ctm_handle h, const double* A, const double* B, const ctm_env* env,

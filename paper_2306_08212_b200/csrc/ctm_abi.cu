@@ -90,6 +90,7 @@ Site site_top(Handle& h, const double* X, int d, int D) { return make_site(h, X,
 
 struct Iso {
   Ten v1, v2;   // v1 (P, D, n1), v2 (n1, D, n2)
+  double gap1 = std::numeric_limits<double>::infinity();   // stage one sigma_n1 / sigma_{n1+1}
 };
 
 // ---------------------------------------------------------------------------------------
@@ -197,7 +198,7 @@ Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool sid
   const int n1 = std::min(c1, P * K);
   Iso r;
   r.v1 = alloc(h, {P, K, n1});
-  svd_left(h, Qt.p, P * K, Bd * F, n1, r.v1.p);
+  r.gap1 = svd_left(h, Qt.p, P * K, Bd * F, n1, r.v1.p);
   Ten Q2 = alloc(h, {n1, Bd, F});
   contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
   const int n2 = std::min(c2, n1 * Bd);
@@ -279,6 +280,7 @@ void run_parallel(Handle& h, std::vector<std::function<void()>>& tasks) {
   for (size_t i = 0; i < tasks.size(); ++i)
     th.emplace_back([&, i]() {
       try {
+        CTM_CUDA(cudaSetDevice(h.device));   // a new host thread starts on device 0
         tasks[i]();
       } catch (...) {
         errs[i] = std::current_exception();
@@ -352,7 +354,15 @@ void reserve_side_cache(Handle& h, const ctm_env* env, SideCache& c) {
   }
 }
 
-void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2], SideCache* cache = nullptr) {
+// On a worker error every sub-stream is drained before the exception leaves: the other
+// chain may still have work in flight (the side-cache copy into the main arena included),
+// and the caller's next call reuses the arena on h.stream with no ordering against them.
+void drain_subs(Handle& h) {
+  for (auto& s : h.subs) cudaStreamSynchronize(s->stream);
+}
+
+void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2], int absorption,
+                    SideCache* cache = nullptr) {
   const ctm_params& p = h.prm;
   const int D = p.D;
   for (auto& s : h.subs) {
@@ -380,6 +390,7 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
       side[2 * x + 1] = side_ts(sub, ri[x], false, p.chi_pp);
       if (cache != nullptr) {
         const SideOut& o = side[2 * x + 1];
+        cache->side[x].v.gap1 = o.v.gap1;
         Ten* dst[3] = {&cache->side[x].v.v1, &cache->side[x].v.v2, &cache->side[x].Q2};
         const Ten* src[3] = {&o.v.v1, &o.v.v2, &o.Q2};
         for (int t = 0; t < 3; ++t) {
@@ -418,9 +429,22 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
       for (int x = 0; x < 2; ++x) right_task(x);
     for (int x = 0; x < 2; ++x) chain_task(x);
   } else {
-    run_parallel(h, T);
+    try {
+      run_parallel(h, T);
+    } catch (...) {
+      drain_subs(h);
+      throw;
+    }
   }
   if (cache != nullptr) cache->valid = true;
+  if (!h.dry) {   // per-cut gaps: main TS [ab, ba], side TS [a-l, a-r, b-l, b-r]
+    for (int c = 0; c < 2; ++c) {
+      const Iso& v = c == 0 ? V[0][1] : V[1][0];
+      h.cut_gap[absorption][c] = std::min(h.cut_gap[absorption][c], v.gap1);
+    }
+    for (int i = 0; i < 4; ++i)
+      h.side_gap[absorption][i] = std::min(h.side_gap[absorption][i], side[i].v.gap1);
+  }
   for (auto& s : h.subs) {
     if (!h.dry) {
       CTM_CUDA(cudaEventRecord(s->ev[1], s->stream));   // join
@@ -616,110 +640,6 @@ void check_env(const ctm_env* e, const ctm_params& p) {
     }
 }
 
-// ---------------------------------------------------------------------------------------
-// Row a10: one column absorption (P:L43), both row-parity windows from one snapshot.
-//   C_y^1 <- N[C_x^1 T_x^2 V_yx] ; T_y^1 <- N[V_xy T_x^1 X X* V_yx] ; C_x^4 <- N[V_yx C_y^4 T_y^4]
-// ---------------------------------------------------------------------------------------
-void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* env, const double* iso_in,
-                       double* iso_out, int absorption, SideCache* cache = nullptr) {
-  const ctm_params& p = h.prm;
-  const int D = p.D;
-  const size_t mark = h.ws.top;
-  Iso V[2][2];   // V[x][y] = projector of cut 'xy' (x above)
-  if (iso_in) {
-    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
-    for (int c = 0; c < 2; ++c) {   // c = 0: ab, 1: ba
-      const double* base = iso_in + (size_t)(absorption * 2 + c) * (n1 + n2);
-      Iso& v = c == 0 ? V[0][1] : V[1][0];
-      v.v1 = Ten{const_cast<double*>(base), {p.chi, D, p.chi_p}};
-      v.v2 = Ten{const_cast<double*>(base + n1), {p.chi_p, D, p.chi}};
-    }
-  } else {
-    isometry_stage(h, env, st, V, cache);
-  }
-  if (iso_out) {
-    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
-    for (int c = 0; c < 2; ++c) {
-      Iso& v = c == 0 ? V[0][1] : V[1][0];
-      if (v.v1.size() != n1 || v.v2.size() != n2) throw Error(CTM_E_ARG, "iso_out needs square extents chi");
-      double* base = iso_out + (size_t)(absorption * 2 + c) * (n1 + n2);
-      if (!h.dry) {
-        CTM_CUDA(cudaMemcpyAsync(base, v.v1.p, n1 * 8, cudaMemcpyDeviceToDevice, h.stream));
-        CTM_CUDA(cudaMemcpyAsync(base + n1, v.v2.p, n2 * 8, cudaMemcpyDeviceToDevice, h.stream));
-      }
-    }
-  }
-  // new tensors (snapshot semantics: written to workspace, committed at the end)
-  double* ss = h.ws.take(6 * (size_t)CTM_SS_SLOTS);   // per-tile sum-of-squares partials
-  Ten nT[2], nC1[2], nC4[2];
-  std::vector<ChainJob> jobs;
-  for (int x = 0; x < 2; ++x) {
-    const int y = 1 - x;
-    Iso& vxy = V[x][y];
-    Iso& vyx = V[y][x];
-    nT[y] = alloc(h, {vxy.v2.ext[2], D, D, vyx.v2.ext[2]});
-    nC1[y] = alloc(h, {vyx.v2.ext[2], envT(env, x, 2, D).ext[3]});
-    nC4[x] = alloc(h, {envT(env, y, 4, D).ext[0], vyx.v2.ext[2]});
-  }
-  Ten T1[2] = {envT(env, 0, 1, D), envT(env, 1, 1, D)};
-  for (int x = 0; x < 2; ++x) {
-    const int y = 1 - x;
-    jobs.push_back(ChainJob{&T1[x], &sl[x], &V[x][y], &V[y][x], &nT[y], ss + (size_t)y * CTM_SS_SLOTS});
-  }
-  std::vector<int> np_t = chains(h, jobs);   // jobs[x] produces nT[y]
-  std::vector<CornerJob> tl, bl;
-  for (int x = 0; x < 2; ++x) {
-    const int y = 1 - x;
-    tl.push_back(CornerJob{envC(env, x, 1), envT(env, x, 2, D), &V[y][x], &nC1[y], ss + (size_t)(2 + y) * CTM_SS_SLOTS});
-    bl.push_back(CornerJob{envC(env, y, 4), envT(env, y, 4, D), &V[y][x], &nC4[x], ss + (size_t)(4 + x) * CTM_SS_SLOTS});
-  }
-  std::vector<int> np_tl = corners(h, tl, true);   // tl[x] -> nC1[y]
-  std::vector<int> np_bl = corners(h, bl, false);  // bl[x] -> nC4[x]
-  std::vector<int> nparts = {np_t[1], np_t[0], np_tl[1], np_tl[0], np_bl[0], np_bl[1]};
-  // K7: normalise + commit (reading R13)
-  if (!h.dry) {
-    std::vector<const double*> src;
-    std::vector<double*> dst;
-    std::vector<size_t> n;
-    for (int y = 0; y < 2; ++y) {
-      src.push_back(nT[y].p);
-      dst.push_back(env->T[y][0]);
-      n.push_back(nT[y].size());
-    }
-    for (int y = 0; y < 2; ++y) {
-      src.push_back(nC1[y].p);
-      dst.push_back(env->C[y][0]);
-      n.push_back(nC1[y].size());
-    }
-    for (int x = 0; x < 2; ++x) {
-      src.push_back(nC4[x].p);
-      dst.push_back(env->C[x][3]);
-      n.push_back(nC4[x].size());
-    }
-    scale_commit(h, src, dst, n, ss, nparts);
-    if (p.flags & CTM_FLAG_CHECK_FINITE) {
-      int* cnt = reinterpret_cast<int*>(h.dev_scalars);
-      CTM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), h.stream));
-      for (size_t i = 0; i < dst.size(); ++i) nonfinite_count(h, dst[i], n[i], cnt);
-      int hc = 0;
-      CTM_CUDA(cudaMemcpyAsync(&hc, cnt, sizeof(int), cudaMemcpyDeviceToHost, h.stream));
-      CTM_CUDA(cudaStreamSynchronize(h.stream));
-      if (hc) throw Error(CTM_E_NONFINITE, "non-finite entries after column absorption " + std::to_string(absorption));
-    }
-  }
-  for (int y = 0; y < 2; ++y) {
-    env->ext[y][4][0] = nT[y].ext[0];
-    env->ext[y][4][1] = nT[y].ext[3];
-    env->ext[y][0][0] = nC1[y].ext[0];
-    env->ext[y][0][1] = nC1[y].ext[1];
-  }
-  for (int x = 0; x < 2; ++x) {
-    env->ext[x][3][0] = nC4[x].ext[0];
-    env->ext[x][3][1] = nC4[x].ext[1];
-  }
-  h.ws.reset(mark);
-}
-
 // Normalise (Frobenius, reading R13) and commit the six new tensors of an absorption.
 void commit_six(Handle& h, ctm_env* env, Ten nT[2], Ten nC1[2], Ten nC4[2], const double* ss,
                 const std::vector<int>& nparts, int absorption) {
@@ -766,6 +686,70 @@ void commit_six(Handle& h, ctm_env* env, Ten nT[2], Ten nC1[2], Ten nC4[2], cons
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Row a10: one column absorption (P:L43), both row-parity windows from one snapshot.
+//   C_y^1 <- N[C_x^1 T_x^2 V_yx] ; T_y^1 <- N[V_xy T_x^1 X X* V_yx] ; C_x^4 <- N[V_yx C_y^4 T_y^4]
+// ---------------------------------------------------------------------------------------
+void column_absorption(Handle& h, const Site sl[2], const Site st[2], ctm_env* env, const double* iso_in,
+                       double* iso_out, int absorption, SideCache* cache = nullptr) {
+  const ctm_params& p = h.prm;
+  const int D = p.D;
+  const size_t mark = h.ws.top;
+  Iso V[2][2];   // V[x][y] = projector of cut 'xy' (x above)
+  if (iso_in) {
+    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
+    for (int c = 0; c < 2; ++c) {   // c = 0: ab, 1: ba
+      const double* base = iso_in + (size_t)(absorption * 2 + c) * (n1 + n2);
+      Iso& v = c == 0 ? V[0][1] : V[1][0];
+      v.v1 = Ten{const_cast<double*>(base), {p.chi, D, p.chi_p}};
+      v.v2 = Ten{const_cast<double*>(base + n1), {p.chi_p, D, p.chi}};
+    }
+  } else {
+    isometry_stage(h, env, st, V, absorption, cache);
+  }
+  if (iso_out) {
+    const size_t n1 = (size_t)p.chi * D * p.chi_p, n2 = (size_t)p.chi_p * D * p.chi;
+    for (int c = 0; c < 2; ++c) {
+      Iso& v = c == 0 ? V[0][1] : V[1][0];
+      if (v.v1.size() != n1 || v.v2.size() != n2) throw Error(CTM_E_ARG, "iso_out needs square extents chi");
+      double* base = iso_out + (size_t)(absorption * 2 + c) * (n1 + n2);
+      if (!h.dry) {
+        CTM_CUDA(cudaMemcpyAsync(base, v.v1.p, n1 * 8, cudaMemcpyDeviceToDevice, h.stream));
+        CTM_CUDA(cudaMemcpyAsync(base + n1, v.v2.p, n2 * 8, cudaMemcpyDeviceToDevice, h.stream));
+      }
+    }
+  }
+  // new tensors (snapshot semantics: written to workspace, committed at the end)
+  double* ss = h.ws.take(6 * (size_t)CTM_SS_SLOTS);   // per-tile sum-of-squares partials
+  Ten nT[2], nC1[2], nC4[2];
+  std::vector<ChainJob> jobs;
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    Iso& vxy = V[x][y];
+    Iso& vyx = V[y][x];
+    nT[y] = alloc(h, {vxy.v2.ext[2], D, D, vyx.v2.ext[2]});
+    nC1[y] = alloc(h, {vyx.v2.ext[2], envT(env, x, 2, D).ext[3]});
+    nC4[x] = alloc(h, {envT(env, y, 4, D).ext[0], vyx.v2.ext[2]});
+  }
+  Ten T1[2] = {envT(env, 0, 1, D), envT(env, 1, 1, D)};
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    jobs.push_back(ChainJob{&T1[x], &sl[x], &V[x][y], &V[y][x], &nT[y], ss + (size_t)y * CTM_SS_SLOTS});
+  }
+  std::vector<int> np_t = chains(h, jobs);   // jobs[x] produces nT[y]
+  std::vector<CornerJob> tl, bl;
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    tl.push_back(CornerJob{envC(env, x, 1), envT(env, x, 2, D), &V[y][x], &nC1[y], ss + (size_t)(2 + y) * CTM_SS_SLOTS});
+    bl.push_back(CornerJob{envC(env, y, 4), envT(env, y, 4, D), &V[y][x], &nC4[x], ss + (size_t)(4 + x) * CTM_SS_SLOTS});
+  }
+  std::vector<int> np_tl = corners(h, tl, true);   // tl[x] -> nC1[y]
+  std::vector<int> np_bl = corners(h, bl, false);  // bl[x] -> nC4[x]
+  std::vector<int> nparts = {np_t[1], np_t[0], np_tl[1], np_tl[0], np_bl[0], np_bl[1]};
+  commit_six(h, env, nT, nC1, nC4, ss, nparts, absorption);   // K7 (reading R13)
+  h.ws.reset(mark);
+}
+
 // REDUCED column absorption (P:L43 with P:L53's projectors): the two cut types' exact
 // reduced environments and one-shot isometries run concurrently on worker sub-handles 0/1.
 void column_absorption_reduced(Handle& h, const Site sl[2], const double* raw[2], ctm_env* env, int absorption) {
@@ -797,7 +781,12 @@ void column_absorption_reduced(Handle& h, const Site sl[2], const double* raw[2]
       }
       V[x][y] = one_shot_isometry(s, M, p.chi);
     });
-  run_parallel(h, tasks);
+  try {
+    run_parallel(h, tasks);
+  } catch (...) {
+    drain_subs(h);
+    throw;
+  }
   for (int i = 0; i < 2; ++i) {
     Handle& s = *h.subs[i];
     if (!h.dry) {
@@ -1054,10 +1043,10 @@ void site_spins_impl(Handle& h, const double* A, const double* B, const ctm_env*
   if (h.prm.d != 2) throw Error(CTM_E_UNSUPPORTED, "site spins are defined for d = 2 (spin 1/2)");
   const size_t mark = h.ws.top;
   Ten rho = bond_rho_raw(h, A, B, env);
-  double* o = h.ws.take(4);
+  double* o = h.ws.take(5);
   site_spins(h, rho.p, o);
   if (!h.dry) {
-    CTM_CUDA(cudaMemcpyAsync(out_host, o, 4 * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaMemcpyAsync(out_host, o, 5 * sizeof(double), cudaMemcpyDeviceToHost, h.stream));
     CTM_CUDA(cudaStreamSynchronize(h.stream));
   }
   h.ws.reset(mark);
@@ -1083,6 +1072,19 @@ int guarded(ctm_handle hh, F&& f) {
   if (!hh) return CTM_E_ARG;
   Handle& h = hh->h;
   h.last_error.clear();
+  // run on the handle's device; the caller's current device is restored on return
+  int prev = -1;
+  cudaGetDevice(&prev);
+  if (prev != h.device && cudaSetDevice(h.device) != cudaSuccess) {
+    h.last_error = "cudaSetDevice failed";
+    return CTM_E_CUDA;
+  }
+  struct Restore {
+    int prev, cur;
+    ~Restore() {
+      if (prev >= 0 && prev != cur) cudaSetDevice(prev);
+    }
+  } restore{prev, h.device};
   try {
     f(h);
     return CTM_OK;
@@ -1115,6 +1117,10 @@ void begin_call(Handle& h) {
   h.prof_ms_subs = 0.0;
   h.prof_flops_subs = 0.0;
   h.prof_n_subs = 0;
+  for (auto& r : h.cut_gap)
+    for (double& g : r) g = std::numeric_limits<double>::infinity();
+  for (auto& r : h.side_gap)
+    for (double& g : r) g = std::numeric_limits<double>::infinity();
   if (!h.dry && h.ws.base == nullptr) throw Error(CTM_E_ARG, "workspace not set (ctm_set_workspace)");
   h.ws.reset(0);
 }
@@ -1137,6 +1143,10 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->ms_gemm = h.prof_ms_subs;
   st->gemm_flops = h.prof_flops_subs;
   st->gemm_launches = h.prof_used + h.prof_n_subs;
+  for (int a = 0; a < 2; ++a) {
+    for (int c = 0; c < 2; ++c) st->cut_gap[a][c] = h.cut_gap[a][c];
+    for (int i = 0; i < 4; ++i) st->side_gap[a][i] = h.side_gap[a][i];
+  }
   if (h.prof_used) {
     CTM_CUDA(cudaEventSynchronize(h.prof_ev[2 * h.prof_used - 1]));
     for (int i = 0; i < h.prof_used; ++i) {
@@ -1231,6 +1241,7 @@ void init_solver(Handle& h, const ctm_params* p) {
   cusolverDnXgesvdjSetTolerance(h.gesvdj_info, tol);
   cusolverDnXgesvdjSetMaxSweeps(h.gesvdj_info, 100);
   cusolverDnSetStream(h.solver, h.stream);
+  ctm::tc_init_kernels();   // per-device attributes, before any worker thread exists
   ctm::iso_init_kernels();
   CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
   h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
@@ -1278,11 +1289,13 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
     warn = CTM_W_CLAMPED;
   }
   h.stream = reinterpret_cast<cudaStream_t>(stream);
+  if (cudaGetDevice(&h.device) != cudaSuccess) return CTM_E_CUDA;   // the handle's device
   try {
     init_solver(h, &h.prm);
     for (int i = 0; i < 4; ++i) {   // workers of the isometry stage (4 side TS, 2 main TS)
       std::unique_ptr<Handle> s(new Handle());
-      s->prm = h.prm;   // (CTM_FLAG_PROFILE kept: the solver's GEMMs are timed too)
+      s->prm = h.prm;
+      s->device = h.device;   // (CTM_FLAG_PROFILE kept: the solver's GEMMs are timed too)
       CTM_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
       s->owns_stream = true;
       init_solver(*s, &s->prm);
@@ -1326,9 +1339,13 @@ int ctm_set_stream(ctm_handle hh, uintptr_t stream) {
 
 int ctm_destroy(ctm_handle hh) {
   if (!hh) return CTM_E_ARG;
+  int prev = -1;
+  cudaGetDevice(&prev);
+  cudaSetDevice(hh->h.device);
   cudaStreamSynchronize(hh->h.stream);
   destroy_handle(hh->h);
   delete hh;
+  if (prev >= 0) cudaSetDevice(prev);
   return CTM_OK;
 }
 

@@ -87,6 +87,11 @@ struct Handle {
   double jacobi_cta_ms = 0.0;           // launch time x CTAs (1 CTA per SM): SM-weighted time
   int n_jacobi = 0;
   int n_kernels = 0;
+  // per-cut truncation gaps of the call (min over its moves; +inf when nothing truncated):
+  // main TS stage one, [absorption][cut ab, ba]; side TS stage one, [absorption][a-l, a-r, b-l, b-r]
+  double cut_gap[2][2] = {{1e300, 1e300}, {1e300, 1e300}};
+  double side_gap[2][4] = {{1e300, 1e300, 1e300, 1e300}, {1e300, 1e300, 1e300, 1e300}};
+  int device = 0;                       // CUDA device the handle (and its workers) run on
   bool dry = false;                     // sizing pass: no launches
   // CTM_FLAG_PROFILE: event pairs around each tc_gemm launch
   std::vector<cudaEvent_t> prof_ev;
@@ -108,6 +113,9 @@ struct Handle {
 constexpr int CTM_SS_SLOTS = 4096;
 int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
              double alpha = 1.0);
+// Per-device one-time kernel attributes (dynamic shared memory > 48 KB): called by ctm_init
+// on the handle's device before any worker thread exists (thread-safe, once per device).
+void tc_init_kernels();
 
 // kernels.cu
 void permute(Handle& h, const double* src, const std::vector<int>& ext, const std::vector<int>& perm,
@@ -121,7 +129,7 @@ void scale_commit(Handle& h, const std::vector<const double*>& srcs, const std::
 void nonfinite_count(Handle& h, const double* p, size_t n, int* dev_count);
 void abs_copy(Handle& h, const double* src, double* dst, size_t n);
 void dot(Handle& h, const double* a, const double* b, size_t n, double* out);
-// rho (2,2,2,2) of the H bond -> (<Sx>_A, <Sz>_A, <Sx>_B, <Sz>_B) into out (device, 4 doubles)
+// rho (2,2,2,2) of the H bond -> (<Sx>_A, <Sz>_A, <Sx>_B, <Sz>_B, m_s) into out (device, 5 doubles)
 void site_spins(Handle& h, const double* rho, double* out);   // out = a.b (device)
 // rho (d,d,d,d) -> symmetrised, trace-normalised; e = Tr(rho h) into e_dev; rho_out nullable
 void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* rho_out, double* e_dev);

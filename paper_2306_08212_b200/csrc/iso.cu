@@ -29,6 +29,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <limits>
+#include <mutex>
+#include <set>
 #include <vector>
 
 #include "ctm_internal.h"
@@ -270,9 +272,13 @@ struct Solver {
 
 }  // namespace
 
-void iso_init_kernels() {
-  static bool done = false;
-  if (done) return;
+void iso_init_kernels() {   // per device, once (see tc_init_kernels)
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  CTM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(dev)) return;
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
   set_smem((const void*)chol_kernel, chol_smem_bytes(LMAX));
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
@@ -280,7 +286,7 @@ void iso_init_kernels() {
   set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<1, 8, 128>, JacCfg<1, 8, 128>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<8, 4, LMAX_BIG>, JacCfg<8, 4, LMAX_BIG>::SMEM);
-  done = true;
+  done.insert(dev);
 }
 
 // Which path takes an R x C truncation to n_keep columns: 0 none (cuSOLVER), 1 direct tall

@@ -162,6 +162,8 @@ __global__ void site_spins_kernel(const double* __restrict__ rho, double* __rest
     out[2 * i] = 0.5 * (r[0][1] + r[1][0]) / tr;        // Tr(rho_sym sigma_x) / 2
     out[2 * i + 1] = 0.5 * (r[0][0] - r[1][1]) / tr;    // Tr(rho sigma_z) / 2
   }
+  // staggered magnetisation m_s = (|<S>_A| + |<S>_B|) / 2 (reading R23)
+  out[4] = 0.5 * (sqrt(out[0] * out[0] + out[1] * out[1]) + sqrt(out[2] * out[2] + out[3] * out[3]));
 }
 
 int grid_for(long long n, int threads = 256) {

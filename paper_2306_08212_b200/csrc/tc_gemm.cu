@@ -4,6 +4,8 @@
 #include <cstdlib>
 #include <cmath>
 #include <map>
+#include <mutex>
+#include <set>
 
 #include "ctm_internal.h"
 
@@ -85,12 +87,7 @@ ModeOut build_modes(std::vector<Leg> legs, int key, int op1, int op2) {
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
 void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CTM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
-    attr_set = true;
-  }
+  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>;   // attributes: tc_init_kernels
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
   launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
@@ -106,6 +103,22 @@ void launch_cfg(Handle& h, const TcArgs& a, int gz) {
     if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, true>(h, a, gz);
     else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, false>(h, a, gz);
   }
+}
+
+// Dynamic shared memory above 48 KB is a per-device function attribute: set it for every
+// instantiation once per device (ctm_init, before any worker thread launches).
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
+void set_attr_cfg2() {
+  using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
+  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
+}
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+void set_attr_cfg() {
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, true>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, false>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, true>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, false>();
 }
 
 struct CfgInfo {
@@ -126,6 +139,19 @@ void launch_idx(Handle& h, int idx, const TcArgs& a, int gz) {
 }
 
 }  // namespace
+
+void tc_init_kernels() {
+  static std::mutex mu;
+  static std::set<int> done;
+  int dev = 0;
+  CTM_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(dev)) return;
+  set_attr_cfg<128, 64, 16, 4, 2, 3, 2>();
+  set_attr_cfg<64, 128, 16, 2, 4, 3, 2>();
+  set_attr_cfg<64, 64, 16, 2, 2, 3, 3>();
+  done.insert(dev);
+}
 
 int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C, double alpha) {
   const int batch = (int)C.p.size();
@@ -286,6 +312,15 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
       best = i;
       best_splits = splits;
     }
+  }
+  if (!C.sumsq.empty() && best_splits == 1) {
+    // the fused sum of squares writes one partial per output tile into a CTM_SS_SLOTS slot
+    // range (the split-K path writes one per reduction CTA, <= 2 x 148): refuse a launch
+    // that would overflow into the neighbouring slots (fails in ctm_init's sizing pass)
+    const long long tiles = ((M + kCfgs[best].BM - 1) / kCfgs[best].BM) * ((N + kCfgs[best].BN - 1) / kCfgs[best].BN);
+    if (tiles > CTM_SS_SLOTS)
+      throw Error(CTM_E_ARG, "contract: " + std::to_string(tiles) + " output tiles exceed the " +
+                                 std::to_string(CTM_SS_SLOTS) + " sum-of-squares slots (chi D too large)");
   }
   if (h.dry) {
     // sizing pass: reserve exactly the split-K slab the real launch will take (the tile /

@@ -51,10 +51,15 @@ class ctm_move_stats(ctypes.Structure):
                 ("min_gap", c_double), ("n_svd", c_int), ("n_kernels", c_int), ("ms_gemm", c_double),
                 ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double),
                 ("n_svd_fallback", c_int), ("ms_jacobi", c_double), ("jacobi_flops", c_double),
-                ("n_jacobi", c_int), ("jacobi_cta_ms", c_double)]
+                ("n_jacobi", c_int), ("jacobi_cta_ms", c_double),
+                ("cut_gap", (c_double * 2) * 2), ("side_gap", (c_double * 4) * 2)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        out = {}
+        for k, _ in self._fields_:
+            v = getattr(self, k)
+            out[k] = [list(r) for r in v] if k in ("cut_gap", "side_gap") else v
+        return out
 
 
 _lib = None
@@ -130,7 +135,8 @@ class CtmHandle:
                                  CTM_SEQUENTIAL if strategy is None else strategy, svd_algo, svd_tol, flags)
         h = c_void_p()
         ws = c_size_t()
-        rc = lib().ctm_init(byref(h), byref(self.params), self.stream.cuda_stream, byref(ws))
+        with torch.cuda.device(self.device):   # the handle lives on (and records) this device
+            rc = lib().ctm_init(byref(h), byref(self.params), self.stream.cuda_stream, byref(ws))
         if rc not in (CTM_OK, CTM_W_CLAMPED):
             raise CtmError(rc, "ctm_init failed")
         self.clamped = rc == CTM_W_CLAMPED
@@ -193,11 +199,9 @@ class CtmHandle:
 
     def ctm_site_spins(self, A, B, env):
         """((Sx_A, Sz_A), (Sx_B, Sz_B)) and m_s = (|<S>_A| + |<S>_B|) / 2."""
-        o = (c_double * 4)()
+        o = (c_double * 5)()
         self._check(lib().ctm_site_spins(self.h, _ptr(A), _ptr(B), byref(env.c), o))
-        sa, sb = (o[0], o[1]), (o[2], o[3])
-        ms = 0.5 * ((sa[0] ** 2 + sa[1] ** 2) ** 0.5 + (sb[0] ** 2 + sb[1] ** 2) ** 0.5)
-        return (sa, sb), ms
+        return ((o[0], o[1]), (o[2], o[3])), o[4]   # m_s computed on the device (out[4])
 
     def ctm_iterate(self, A, B, env, n_iter):
         st = ctm_move_stats()

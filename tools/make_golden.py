@@ -1,7 +1,7 @@
 """Write tests/golden/oracle_*.json: gauge-invariant oracle outputs for the small configs.
 
-Calls ONLY oracle/ and ctm_inputs (never the CUDA path).  Used as the expected values of
-smoke() and as a regression fixture for the oracle itself.  Re-run after any change to
+Calls ONLY oracle/ and ctm_inputs (never the CUDA path).  Read by
+tests/test_oracle_golden.py as a regression fixture of the oracle itself.  Re-run after any change to
 the oracle's arithmetic (and say why in the commit message)."""
 import json
 import os
