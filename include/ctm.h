@@ -91,6 +91,12 @@ extern "C" {
 #define CTM_RENV_APPROX 0    /* {C'^1, T'^2, C'^2} with side isometries */
 #define CTM_RENV_EXACT 1     /* exact Fig 3(b) network, P:L53 (NEXT on GPU)            */
 
+/* two-stage isometry modes (ctm_ts_isometry) */
+#define CTM_TS_MAIN 0        /* both stages are SVDs (left singular vectors, sign rule)     */
+#define CTM_TS_SIDE 1        /* a stage two that truncates nothing returns an orthonormal
+                                basis of its column space (reading R24: the side isometries
+                                only build M, where that basis cancels)                     */
+
 /* bonds (ctm_bond_energy) */
 #define CTM_BOND_H 0         /* A left of B: 2x1 window                               */
 #define CTM_BOND_V 1         /* A above B: 1x2 window                                 */
@@ -189,6 +195,22 @@ int ctm_reduced_env(ctm_handle h, const double* C1, const double* T2, const doub
                     const double* T1, const double* X, const double* Xbra, const double* T3,
                     int mode, double* M_out, double* iso_out);
 
+/* ctm_ts_isometry: the two-stage isometry TS(Q; c1, c2) of P:L60 ("we reshape it to matrix
+ * of dimension chi D x chi D ... take the first chi' left singular vectors as U_d^1 ...
+ * additional SVD on (chi' D, chi) matrix to obtain U_d^2"), rows a2 (side) and a5
+ * (main) of SURVEY 8(a), on a caller tensor:
+ *   Q (P, K, B, F) row-major device, P <= chi, K = B = D, F <= chi (the handle's sizing);
+ *   stage one: v1 (P, K, n1) = first n1 = min(c1, P K) left singular vectors of Q as
+ *              (P K) x (B F);   c1 <= max(chi', chi'');
+ *   stage two: v2 (n1, B, n2) = first n2 = min(c2, n1 B) left singular vectors of
+ *              Q2 = v1^T Q as (n1 B) x F;   c2 <= chi.
+ *   v1_out, v2_out: device, caller-owned.  gaps_host (nullable, 2 doubles): the stage gaps
+ *   sigma_n / sigma_{n+1} (+inf where nothing is truncated).
+ *   mode CTM_TS_MAIN / CTM_TS_SIDE (above).  Synchronises the stream.  The same routine the
+ *   move runs for every cut (the a5 parity tests call it on a given M). */
+int ctm_ts_isometry(ctm_handle h, const double* Q, int P, int K, int B, int F, int c1, int c2, int mode,
+                    double* v1_out, double* v2_out, double* gaps_host);
+
 /* ctm_absorb_truncate: SURVEY rows a6-a8 (Fig 4(b)): ket absorption,
  * v1 truncation, bra absorption, v2 truncation, in six contractions S1..S6.
  *   T      (chi, D, D, chi)      as (in, k_face, b_face, out)
@@ -217,9 +239,11 @@ int ctm_left_move(ctm_handle h, const double* A, const double* B, ctm_env* env,
 /* ctm_move: the move in direction dir (CTM_LEFT/RIGHT/UP/DOWN) = relabel the
  * environment by quarter turns (clockwise storage: no data movement), permute the
  * site legs on the device, left move, turn back ("moves in other directions
- * can be adjusted accordingly").  ctm_iterate runs n_iter x (left, right, up, down). */
+ * can be adjusted accordingly").  iso_out (nullable): the move's isometries in the rotated
+ * (left-move) picture, layout as ctm_left_move's.  ctm_iterate runs n_iter x (left, right,
+ * up, down). */
 int ctm_move(ctm_handle h, int dir, const double* A, const double* B, ctm_env* env,
-             ctm_move_stats* st);
+             double* iso_out, ctm_move_stats* st);
 /* ctm_converge: CTM iterations (left, right, up, down) until the corner spectra move by
  * less than tol between iterations, at most max_iter ("N_CTM ~ 10-30 times, the
  * environment tensors will become sufficiently converged").  Criterion (DESIGN.md reading

@@ -91,6 +91,7 @@ Site site_top(Handle& h, const double* X, int d, int D) { return make_site(h, X,
 struct Iso {
   Ten v1, v2;   // v1 (P, D, n1), v2 (n1, D, n2)
   double gap1 = std::numeric_limits<double>::infinity();   // stage one sigma_n1 / sigma_{n1+1}
+  double gap2 = std::numeric_limits<double>::infinity();   // stage two (inf: nothing truncated)
 };
 
 // ---------------------------------------------------------------------------------------
@@ -203,7 +204,7 @@ Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool sid
   contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
   const int n2 = std::min(c2, n1 * Bd);
   r.v2 = alloc(h, {n1, Bd, n2});
-  svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p, side);
+  r.gap2 = svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p, side);
   if (Q2_keep) *Q2_keep = Q2;
   return r;
 }
@@ -869,11 +870,11 @@ void rotate_site(Handle& h, const double* X, double* out, int turns) {
   permute(h, X, {h.prm.d, h.prm.D, h.prm.D, h.prm.D, h.prm.D}, {pm[0], pm[1], pm[2], pm[3], pm[4]}, out);
 }
 
-void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env) {
+void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env, double* iso_out = nullptr) {
   static const int turns_for[4] = {0, 2, 3, 1};   // LEFT, RIGHT, UP, DOWN: cw turns bringing it left
   const int n = turns_for[dir];
   if (n == 0) {
-    left_move(h, A, B, env, nullptr, nullptr);
+    left_move(h, A, B, env, nullptr, iso_out);
     return;
   }
   const size_t mark = h.ws.top;
@@ -886,7 +887,7 @@ void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env
   }
   for (int i = 0; i < n; ++i) rotate_env_cw(env);
   try {
-    left_move(h, Ar, Br, env, nullptr, nullptr);
+    left_move(h, Ar, Br, env, nullptr, iso_out);
   } catch (...) {
     for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
     throw;
@@ -1198,6 +1199,10 @@ void size_workspace(Handle& h) {
                    {dummy, {c, D, D, c}}, &st};
     ctm::reduced_env(h, ri, p.chi_pp);
     main_need = std::max(main_need, h.ws.peak);
+    h.ws.reset(0);   // ctm_ts_isometry (main TS, chi' -> chi)
+    h.ws.peak = 0;
+    ctm::ts_isometry(h, ri.T1, std::max(p.chi_p, p.chi_pp), p.chi, nullptr, false);
+    main_need = std::max(main_need, h.ws.peak);
     // optional entry points are sized when they fit the kernel's 2^31-element operand
     // limit; otherwise the handle still serves moves and those calls report CTM_E_ARG /
     // CTM_E_NOMEM when made (C5 at chi = 256: the closures' enlarged corners)
@@ -1402,6 +1407,29 @@ int ctm_absorb_truncate(ctm_handle hh, const double* T, const double* X, const d
   });
 }
 
+int ctm_ts_isometry(ctm_handle hh, const double* Q, int P, int K, int Bd, int F, int c1, int c2, int mode,
+                    double* v1_out, double* v2_out, double* gaps_host) {
+  return guarded(hh, [&](Handle& h) {
+    if (!Q || !v1_out || !v2_out) throw Error(CTM_E_ARG, "null pointer");
+    if (mode != CTM_TS_MAIN && mode != CTM_TS_SIDE) throw Error(CTM_E_ARG, "unknown TS mode");
+    const ctm_params& p = h.prm;
+    // the workspace is sized for the TS calls of a move: Q up to (chi, D, D, chi)
+    if (P < 1 || F < 1 || c1 < 1 || c2 < 1 || P > p.chi || F > p.chi || K != p.D || Bd != p.D ||
+        c1 > std::max(p.chi_p, p.chi_pp) || c2 > p.chi)
+      throw Error(CTM_E_ARG, "TS shape outside the handle's (chi, D, D, chi) / chi', chi'' sizing");
+    begin_call(h);
+    ctm::Ten Qt{const_cast<double*>(Q), {P, K, Bd, F}};
+    ctm::Iso v = ctm::ts_isometry(h, Qt, c1, c2, nullptr, mode == CTM_TS_SIDE);
+    CTM_CUDA(cudaMemcpyAsync(v1_out, v.v1.p, v.v1.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
+    CTM_CUDA(cudaMemcpyAsync(v2_out, v.v2.p, v.v2.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    if (gaps_host) {
+      gaps_host[0] = v.gap1;
+      gaps_host[1] = v.gap2;
+    }
+  });
+}
+
 int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const double* C2, const double* T1,
                     const double* X, const double* Xbra, const double* T3, int mode, double* M_out,
                     double* iso_out) {
@@ -1455,13 +1483,14 @@ int ctm_left_move(ctm_handle hh, const double* A, const double* B, ctm_env* env,
   });
 }
 
-int ctm_move(ctm_handle hh, int dir, const double* A, const double* B, ctm_env* env, ctm_move_stats* st) {
+int ctm_move(ctm_handle hh, int dir, const double* A, const double* B, ctm_env* env, double* iso_out,
+             ctm_move_stats* st) {
   return guarded(hh, [&](Handle& h) {
     if (!A || !B || !env || dir < 0 || dir > 3) throw Error(CTM_E_ARG, "bad argument");
     begin_call(h);
     ctm::check_env(env, h.prm);
     CTM_CUDA(cudaEventRecord(h.ev[0], h.stream));
-    ctm::move_dir(h, dir, A, B, env);
+    ctm::move_dir(h, dir, A, B, env, iso_out);
     CTM_CUDA(cudaEventRecord(h.ev[1], h.stream));
     if (st) {
       CTM_CUDA(cudaEventSynchronize(h.ev[1]));

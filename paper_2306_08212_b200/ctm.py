@@ -25,6 +25,7 @@ CTM_FLAG_MOVE_ONLY = 2
 CTM_FLAG_PROFILE = 4
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
+CTM_TS_MAIN, CTM_TS_SIDE = 0, 1
 DIRS = {"left": 0, "right": 1, "up": 2, "down": 3}
 CTM_E_ARG, CTM_E_CUDA, CTM_E_SOLVER, CTM_E_NONFINITE, CTM_E_NOMEM, CTM_E_UNSUPPORTED = 1, 2, 3, 4, 5, 6
 STATUS = {0: "CTM_OK", 1: "CTM_E_ARG", 2: "CTM_E_CUDA", 3: "CTM_E_SOLVER", 4: "CTM_E_NONFINITE",
@@ -83,7 +84,9 @@ def lib():
             "ctm_reduced_env": (c_int, [P, P, P, P, P, P, P, P, c_int, P, P]),
             "ctm_absorb_truncate": (c_int, [P, P, P, P, P, P, P, P, P]),
             "ctm_left_move": (c_int, [P, P, P, POINTER(ctm_env), P, P, POINTER(ctm_move_stats)]),
-            "ctm_move": (c_int, [P, c_int, P, P, POINTER(ctm_env), POINTER(ctm_move_stats)]),
+            "ctm_move": (c_int, [P, c_int, P, P, POINTER(ctm_env), P, POINTER(ctm_move_stats)]),
+            "ctm_ts_isometry": (c_int, [P, P, c_int, c_int, c_int, c_int, c_int, c_int, c_int, P, P,
+                                        POINTER(c_double)]),
             "ctm_iterate": (c_int, [P, P, P, POINTER(ctm_env), c_int, POINTER(ctm_move_stats)]),
             "ctm_converge": (c_int, [P, P, P, POINTER(ctm_env), c_int, c_double, POINTER(c_int), POINTER(c_double),
                                      POINTER(ctm_move_stats)]),
@@ -103,7 +106,7 @@ def lib():
 
 def exported_symbols():
     return ["ctm_abi_version", "ctm_init", "ctm_set_workspace", "ctm_set_stream", "ctm_destroy",
-            "ctm_last_error", "ctm_reduced_env", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
+            "ctm_last_error", "ctm_reduced_env", "ctm_ts_isometry", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
             "ctm_iterate", "ctm_converge", "ctm_site_spins", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
 
 
@@ -183,10 +186,23 @@ class CtmHandle:
                                         byref(st) if stats else None))
         return st.as_dict() if stats else None
 
-    def ctm_move(self, direction, A, B, env):
+    def ctm_move(self, direction, A, B, env, iso_out=None):
         st = ctm_move_stats()
-        self._check(lib().ctm_move(self.h, DIRS[direction], _ptr(A), _ptr(B), byref(env.c), byref(st)))
+        self._check(lib().ctm_move(self.h, DIRS[direction], _ptr(A), _ptr(B), byref(env.c), _ptr(iso_out),
+                                   byref(st)))
         return st.as_dict()
+
+    def ctm_ts_isometry(self, Q, c1, c2, mode=CTM_TS_MAIN):
+        """TS(Q; c1, c2) on a (P, K, B, F) device tensor -> (v1, v2, (gap1, gap2))."""
+        P_, K, B, F = Q.shape
+        n1 = min(c1, P_ * K)
+        n2 = min(c2, n1 * B)
+        torch = self.torch
+        v1 = torch.empty((P_, K, n1), dtype=torch.float64, device=Q.device)
+        v2 = torch.empty((n1, B, n2), dtype=torch.float64, device=Q.device)
+        gaps = (c_double * 2)()
+        self._check(lib().ctm_ts_isometry(self.h, _ptr(Q), P_, K, B, F, c1, c2, mode, _ptr(v1), _ptr(v2), gaps))
+        return v1, v2, (gaps[0], gaps[1])
 
     def ctm_converge(self, A, B, env, max_iter, tol):
         """Returns (iterations, last corner-spectrum distance, stats dict)."""

@@ -1,0 +1,226 @@
+"""Full-size GPU parity against the oracle (BASELINE.json configs at their own sizes).
+
+  * Row a5 (main projectors) and row a2 (side projectors): libctm's TS on
+    a given tensor against the oracle's TS on the SAME tensor, from Tiny up to C5/chi=256
+    (the C5 shapes reach the solver's l > 160 paths: two-block Cholesky, the big-row
+    triangular solve and the 8-CTA cluster Jacobi).  Projectors are gauge-free, so they
+    are compared through their action on random probes.
+  * Shadowed trajectories: along 20 CTM iterations at C2 and C3 and one iteration at C4,
+    every GPU move is shadowed by the oracle from the GPU's own environment before the
+    move: (i) the oracle's projectors vs the GPU's, (ii) the oracle's column absorptions
+    with the GPU's isometries injected vs the GPU's new environment entrywise (1e-11),
+    (iii) the oracle's own move (its own projectors) vs the GPU's through the gauge-free
+    contracted new column, (iv) the closures on the GPU's environment.  This replaces the
+    round-1 "30 x perturbed-oracle spread" bar: each step is held to the north star's
+    tolerance because the comparison never lets two trajectories drift apart.
+
+Projector tolerance: max(1e-9, 1e3 eps (sigma_1/sigma_n) / (1 - sigma_{n+1}/sigma_n)) from
+the oracle's logged spectrum at the cut (first-order perturbation of an invariant subspace
+by a backward error of eps ||M||); every printed line reports the error and the bar.
+"""
+import numpy as np
+import pytest
+
+import ctm_inputs as ci
+from oracle import ctm_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    from paper_2306_08212_b200 import ctm
+DEV = "cuda"
+EPS = 2.220446049250313e-16
+
+
+def T_(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def rel_err(got, ref):
+    return np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-300)
+
+
+def proj_err(a, b, rng, nprobe=8):
+    """max |a a^T x - b b^T x| / max |x| over random probes x (a, b: orthonormal columns)."""
+    X = rng.standard_normal((a.shape[0], nprobe))
+    return float(np.abs(a @ (a.T @ X) - b @ (b.T @ X)).max() / np.abs(X).max())
+
+
+def proj_tol(st):
+    """Bar for a projector of a truncation with oracle stats st (left_singular's record)."""
+    if not np.isfinite(st["gap"]) or st["sigma_last_kept"] <= 0:
+        return 1e-9
+    cond = st["sigma_first"] / st["sigma_last_kept"]
+    return max(1e-9, 1e3 * EPS * cond / (1.0 - 1.0 / st["gap"]))
+
+
+def ts_compare(v1g, v2g, v1r, v2r, st1, rng):
+    """Stage-one projector v1 v1^T and composite V V^T (V = v1 v2) of GPU vs oracle."""
+    n1 = v1r.shape[2]
+    e1 = proj_err(v1g.reshape(-1, n1), v1r.reshape(-1, n1), rng)
+    Vg = np.einsum("pka,abz->pkbz", v1g, v2g)
+    Vr = np.einsum("pka,abz->pkbz", v1r, v2r)
+    n2 = Vr.shape[3]
+    e2 = proj_err(Vg.reshape(-1, n2), Vr.reshape(-1, n2), rng)
+    return e1, e2, proj_tol(st1)
+
+
+# ----------------------------------------------------------------------------------------
+# rows a5 and a2 at every BASELINE size
+# ----------------------------------------------------------------------------------------
+FULL = ["tiny", "c2", "c3", "c4", "c5", "c5_256"]
+
+
+@pytest.mark.parametrize("name", FULL)
+@pytest.mark.parametrize("x", ["a", "b"])
+def test_main_ts_projectors_on_the_same_M(name, x):
+    """Row a5: M = the GPU's approximated reduced environment of cut type x (itself checked
+    entrywise against the oracle's M, 1e-10), then TS(M; chi', chi) by libctm and by the
+    oracle on that same M."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    C, T = g["C"], g["T"]
+    X = g["A"] if x == "a" else g["B"]
+    M_ref, _ = O.reduced_env_approx(C[(x, 1)], T[(x, 2)], C[(x, 2)], T[(x, 1)], X, X, T[(x, 3)], cfg.chi_pp)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    M = torch.empty((cfg.chi, cfg.D, cfg.D, cfg.chi), dtype=torch.float64, device=DEV)
+    h.ctm_reduced_env(T_(C[(x, 1)]), T_(T[(x, 2)]), T_(C[(x, 2)]), T_(T[(x, 1)]), T_(X), T_(X), T_(T[(x, 3)]), M)
+    Mh = M.cpu().numpy()
+    assert rel_err(Mh, M_ref) <= 1e-10
+    v1g, v2g, gaps = h.ctm_ts_isometry(M, cfg.chi_p, cfg.chi, ctm.CTM_TS_MAIN)
+    stats = []
+    v1r, v2r = O.ts_isometry(Mh, cfg.chi_p, cfg.chi, stats)
+    v1g, v2g = v1g.cpu().numpy(), v2g.cpu().numpy()
+    e1, e2, tol = ts_compare(v1g, v2g, v1r, v2r, stats[0], np.random.default_rng(11))
+    print(f"{name} cut {x}: P1 err {e1:.2e}  P err {e2:.2e}  bar {tol:.2e}  gap gpu {gaps[0]:.6f} "
+          f"oracle {stats[0]['gap']:.6f}  s1/sn {stats[0]['sigma_first'] / stats[0]['sigma_last_kept']:.3g}")
+    assert e1 <= tol and e2 <= tol
+    if np.isfinite(stats[0]["gap"]):
+        assert gaps[0] == pytest.approx(stats[0]["gap"], rel=1e-8)
+    for v, n in ((v1g, v1g.shape[2]), (v2g, v2g.shape[2])):
+        m = v.reshape(-1, n)
+        assert np.abs(m.T @ m - np.eye(n)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("name", ["c5", "c5_256"])
+def test_side_ts_projectors_c5(name):
+    """Row a2 at C5 sizes (l = 232 / 288 > 160): TS(C^1 T^1) and TS(C^2 T^3) by libctm
+    (side mode, reading R24) against the oracle's, projectors on probes."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    C, T = g["C"], g["T"]
+    Ql, Qr = O.side_products(C[("a", 1)], T[("a", 1)], C[("a", 2)], T[("a", 3)])
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    rng = np.random.default_rng(5)
+    for Q in (Ql, Qr):
+        v1g, v2g, gaps = h.ctm_ts_isometry(T_(Q), cfg.chi_pp, cfg.chi_pp, ctm.CTM_TS_SIDE)
+        stats = []
+        v1r, v2r = O.ts_isometry(Q, cfg.chi_pp, cfg.chi_pp, stats)
+        e1, e2, tol = ts_compare(v1g.cpu().numpy(), v2g.cpu().numpy(), v1r, v2r, stats[0], rng)
+        print(f"{name} side: P1 err {e1:.2e}  P err {e2:.2e}  bar {tol:.2e}  gap {gaps[0]:.6f}")
+        assert e1 <= tol and e2 <= tol
+
+
+# ----------------------------------------------------------------------------------------
+# shadowed trajectories
+# ----------------------------------------------------------------------------------------
+def _iso_from_flat(p, chi, D, chi_p):
+    n1, n2 = chi * D * chi_p, chi_p * D * chi
+    out, off = [], 0
+    for _ in range(2):
+        proj = {}
+        for cut in ("ab", "ba"):
+            proj[cut] = {"v1": p[off:off + n1].reshape(chi, D, chi_p),
+                         "v2": p[off + n1:off + n1 + n2].reshape(chi_p, D, chi)}
+            off += n1 + n2
+        out.append(proj)
+    return out
+
+
+def _to_left(env, A, B, direction):
+    e, a, b = env, A, B
+    for _ in range(O._TURNS[direction]):
+        e, a, b = O.rotate_cw(e, a, b)
+    return e, a, b
+
+
+def _col_probe(e, x, P1, P2):
+    """The new left column of the window with x on top, contracted along its (new, gauge-
+    dependent) vertical bonds, ket/bra legs closed with fixed random probes: a gauge-free
+    (chi, chi) matrix indexed by the old bonds to T^2 and T^4."""
+    y = O.OTHER[x]
+    c = np.einsum("xR,yklx->Rykl", e["C"][(x, 1)], e["T"][(x, 1)])
+    c = np.einsum("Rykl,kl->Ry", c, P1)
+    c = np.einsum("Ry,zmny->Rzmn", c, e["T"][(y, 1)])
+    c = np.einsum("Rzmn,mn->Rz", c, P2)
+    return np.einsum("Rz,Sz->RS", c, e["C"][(y, 4)])
+
+
+def shadow_move(env_h, A, B, direction, cfg, iso_flat, gpu_after, rng, log):
+    chi, chi_p, chi_pp, D = cfg.chi, cfg.chi_p, cfg.chi_pp, cfg.D
+    e0, a, b = _to_left(env_h, A, B, direction)
+    gpu_isos = _iso_from_flat(iso_flat, chi, D, chi_p)
+    worst = 0.0
+    # (i) projectors, absorption by absorption, from the environment the GPU saw
+    e_inj = e0
+    for ab in range(2):
+        stats = []
+        own = O._cut_projectors(e_inj, a, b, chi, chi_p, chi_pp, "sequential", stats)
+        for k, cut in enumerate(("ab", "ba")):
+            st1 = stats[6 * k + 4]   # per cut type: side l (2 records), side r (2), main (2)
+            e1, e2, tol = ts_compare(gpu_isos[ab][cut]["v1"], gpu_isos[ab][cut]["v2"], own[cut]["v1"],
+                                     own[cut]["v2"], st1, rng)
+            worst = max(worst, max(e1, e2) / tol)
+            assert e1 <= tol and e2 <= tol, (direction, ab, cut, e1, e2, tol)
+        # (ii) the oracle's absorption with the GPU's isometries injected
+        e_inj, _ = O.column_absorption(e_inj, a, b, chi, projectors=gpu_isos[ab])
+    g_left, _, _ = _to_left(gpu_after, A, B, direction)
+    ent = 0.0
+    for kind in ("C", "T"):
+        for key, ref in e_inj[kind].items():
+            ent = max(ent, rel_err(g_left[kind][key], ref))
+    assert ent <= 1e-11, (direction, ent)
+    # (iii) the oracle's own move vs the GPU's: the gauge-free contracted new column
+    e_own = O.left_move(e0, a, b, chi, chi_p, chi_pp)
+    colerr = 0.0
+    for x in ("a", "b"):
+        P1, P2 = rng.standard_normal((D, D)), rng.standard_normal((D, D))
+        colerr = max(colerr, rel_err(_col_probe(g_left, x, P1, P2), _col_probe(e_own, x, P1, P2)))
+    assert colerr <= 1e-9, (direction, colerr)
+    log.append((direction, worst, ent, colerr))
+
+
+@pytest.mark.parametrize("name,n_iter", [("c2", 20), ("c3", 20), ("c4", 1)])
+def test_shadowed_trajectory(name, n_iter):
+    """Every move of n_iter CTM iterations (left, right, up, down) shadowed by
+    the oracle from the GPU's environment; closures on the GPU's environment after each
+    iteration (C4: after the iteration only)."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    A, B = g["A"], g["B"]
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_CHECK_FINITE)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
+    hop = ci.heisenberg_h()
+    rng = np.random.default_rng(3)
+    log = []
+    for it in range(n_iter):
+        for direction in ("left", "right", "up", "down"):
+            before = env.to_host()
+            st = h.ctm_move(direction, T_(A), T_(B), env, iso_out=iso)
+            assert st["n_svd_fallback"] == 0
+            shadow_move(before, A, B, direction, cfg, iso.cpu().numpy(), env.to_host(), rng, log)
+        e_h = env.to_host()
+        for bond, bname in ((ctm.CTM_BOND_H, "H"), (ctm.CTM_BOND_V, "V")):
+            e_gpu = h.ctm_bond_energy(T_(A), T_(B), env, T_(hop), bond)
+            e_ref = O.bond_energy(e_h, A, B, hop, bname)[0]
+            assert abs(e_gpu - e_ref) <= 1e-9 * max(abs(e_ref), 1e-3), (it, bname, e_gpu, e_ref)
+        if name != "c4":
+            v, ratio = h.ctm_norm_2x2(T_(A), T_(B), env)
+            ref = O.norm_2x2(e_h, A, B)
+            assert abs(v - ref) <= 1e-11 * abs(ref) / max(abs(ratio), 1e-6), (it, v, ref, ratio)
+        w = max(r[1] for r in log[-4:])
+        print(f"{name} iteration {it + 1}: worst projector err/bar {w:.3f}, injected-entrywise "
+              f"{max(r[2] for r in log[-4:]):.2e}, own-move column {max(r[3] for r in log[-4:]):.2e}, "
+              f"e_H {e_gpu:.10f}")

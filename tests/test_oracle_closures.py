@@ -203,3 +203,47 @@ def test_site_spins_bounded_for_a_positive_environment():
     g = ci.generate(cfg, "double_layer")
     for x, z in O.site_spins({"C": g["C"], "T": g["T"]}, g["A"], g["B"]):
         assert np.hypot(x, z) <= 0.5 + 1e-12
+
+
+# ----------------------------------------------------------------------------------------
+# reduced_env_exact (Fig 3(a,b)) closed with the rest of its window
+# ----------------------------------------------------------------------------------------
+def _window_3x3_fused(C1, T2, C2, T1, X, Xb, T3, C4, T4, C3):
+    """<psi|psi> of the 3x3 window  C1 T2 C2 / T1 X T3 / C4 T4 C3  (clockwise storage),
+    formulated independently of reduced_env_exact: fused double layer a = sum_s X X* with
+    D^2 legs (ket != bra allowed), fused edges, contracted row by row."""
+    D = X.shape[1]
+    a = np.einsum("sabcd,sefgh->aebfcgdh", X, Xb).reshape(D * D, D * D, D * D, D * D)   # (u, l, d, r)
+    f = lambda t: t.reshape(t.shape[0], D * D, t.shape[3])
+    # top row: C1(d=i, r=p) T2(l=p, j, r=q) C2(l=q, d=k) -> (i, j, k)
+    R = np.einsum("ip,pjq->ijq", C1, f(T2))
+    R = np.einsum("ijq,qk->ijk", R, C2)
+    # middle row: T1(d=I, l, u=i)  a(j, l, J, r)  T3(u=k, r, d=K)
+    R = np.einsum("ijk,Ili->jkIl", R, f(T1))
+    R = np.einsum("jkIl,jlJr->kIJr", R, a)
+    R = np.einsum("kIJr,krK->IJK", R, f(T3))
+    # bottom row: C4(r=m, u=I)  T4(r=n, J, l=m)  C3(u=K, l=n)
+    R = np.einsum("IJK,mI->JKm", R, C4)
+    R = np.einsum("JKm,nJm->Kn", R, f(T4))
+    return float(np.einsum("Kn,Kn->", R, C3))
+
+
+@pytest.mark.parametrize("D,chi,seed", [(2, 4, 51), (3, 5, 52)])
+def test_reduced_env_exact_closes_to_the_window_norm(D, chi, seed):
+    """M_exact(q, k_d, b_d, q') closed with the bottom row C^4 T^4 C^3 equals the 3x3 window
+    norm computed in the fused row-transfer order; ket != bra catches ket/bra mix-ups, random
+    rectangular-free extents catch transposed boundary legs."""
+    rng = np.random.default_rng(seed)
+    d = 2
+    C1, C2, C3, C4 = (rng.standard_normal((chi, chi)) for _ in range(4))
+    T1, T2, T3, T4 = (rng.standard_normal((chi, D, D, chi)) for _ in range(4))
+    X = rng.standard_normal((d, D, D, D, D))
+    Xb = rng.standard_normal((d, D, D, D, D))
+    M = O.reduced_env_exact(C1, T2, C2, T1, X, Xb, T3)
+    # bottom row: C4 (r=m, u=q), T4 (r=n, k, b, l=m), C3 (u=q', l=n)
+    closed = np.einsum("qkbz,mq,nkbm,zn->", M, C4, T4, C3)
+    want = _window_3x3_fused(C1, T2, C2, T1, X, Xb, T3, C4, T4, C3)
+    assert closed == pytest.approx(want, rel=1e-11)
+    # the closure is not blind to a ket/bra exchange of the down legs
+    closed_swapped = np.einsum("qbkz,mq,nkbm,zn->", M, C4, T4, C3)
+    assert abs(closed_swapped - want) > 1e-6 * abs(want)

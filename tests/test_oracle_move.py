@@ -189,3 +189,72 @@ def test_converge_iterations_monotone_in_tol():
     _, it_tight, d_tight = O.converge(env, g["A"], g["B"], cfg.chi, 1e-8, 30)
     assert it_loose <= it_tight
     assert d_tight < 1e-8 or it_tight == 30
+
+
+# ----------------------------------------------------------------------------------------
+# Reading R5 (which cut gets which projector; "P_ab and P_ba", "v_ba^1 contracts
+# with boundary index of T_a^1 and virtual index of A"): a LOSSLESS TRUNCATION whose two cut
+# types have different exact subspaces, so the assignment decides the result.
+#   * Each site's down leg is rank one: X(s,u,l,d,r) = x(s,u,l,r) w_X(d), w_A != w_B.  The
+#     legs crossing cut 'xy' (x above) -- T^1's boundary leg q and X's down legs (k, b) --
+#     then carry vectors in q-space (x) w_X (x) w_X: exact rank chi0 of chi0 D^2 rows.
+#   * The top edge above x is consistent with the lattice (the site above x is y):
+#     T_x^2(l,k,b,r) = t(l,r) w_Y(k) w_Y(b).
+# With chi = chi0 every truncation keeps chi0 of chi0 D^2 rows and is exact for the right
+# assignment: the new column contracted along its bonds equals old column (x) inserted
+# column.  Swapping V_ab <-> V_ba (same shapes, so only the values can tell) projects X's
+# legs onto w_Y (x) w_Y and the column changes.
+# ----------------------------------------------------------------------------------------
+def _r5_case(seed=77, d=2, D=2, chi0=2):
+    rng = np.random.default_rng(seed)
+    w = {"a": rng.standard_normal(D), "b": rng.standard_normal(D)}
+    site = {}
+    for x in ("a", "b"):
+        core = rng.standard_normal((d, D, D, D))                     # (s, u, l, r)
+        site[x] = np.einsum("sulr,d->suldr", core, w[x])
+        site[x] /= np.linalg.norm(site[x])
+    cfg = ci.custom(d, D, chi0, chi0=chi0, seed_index=78)
+    g = ci.generate(cfg)
+    C, T = dict(g["C"]), dict(g["T"])
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        t = rng.standard_normal((chi0, chi0))
+        T[(x, 2)] = np.einsum("lr,k,b->lkbr", t, w[y], w[y])
+        T[(x, 2)] /= np.linalg.norm(T[(x, 2)])
+    return {"C": C, "T": T}, site["a"], site["b"], chi0
+
+
+@pytest.mark.parametrize("strategy", ["sequential", "reduced"])
+def test_r5_cut_assignment_is_exact_on_a_lossless_truncation(strategy):
+    env, A, B, chi = _r5_case()
+    S = {"a": A, "b": B}
+    stats = []
+    new, proj = O.column_absorption(env, A, B, chi, chi, chi, strategy=strategy, stats=stats)
+    C, T, nC, nT = env["C"], env["T"], new["C"], new["T"]
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        V = proj[x + y]["V"] if strategy == "reduced" else O.compose_isometry(proj[x + y]["v1"], proj[x + y]["v2"])
+        assert V.shape == (chi, 2, 2, chi)   # keeps chi of chi D^2 = 4 chi rows: a real truncation
+        old = col_left(C[(x, 1)], T[(x, 1)], T[(y, 1)], C[(y, 4)])
+        exp = ins_left(old, T[(x, 2)], S[x], S[y], T[(y, 4)])
+        got = col_left(nC[(y, 1)], nT[(y, 1)], nT[(x, 1)], nC[(x, 4)])
+        assert np.allclose(_nrm(got), _nrm(exp), atol=1e-12), np.abs(_nrm(got) - _nrm(exp)).max()
+
+
+@pytest.mark.parametrize("strategy", ["sequential", "reduced"])
+def test_r5_swapped_cut_assignment_fails(strategy):
+    """The deliberately mis-assigned projectors (V_ab at the 'ba' cuts and vice versa) break
+    the same identity: the pin above cannot pass with the wrong reading."""
+    env, A, B, chi = _r5_case()
+    S = {"a": A, "b": B}
+    own = O._cut_projectors(env, A, B, chi, chi, chi, strategy, None)
+    swapped = {"ab": own["ba"], "ba": own["ab"]}
+    new, _ = O.column_absorption(env, A, B, chi, chi, chi, strategy=strategy, projectors=swapped)
+    C, T, nC, nT = env["C"], env["T"], new["C"], new["T"]
+    worst = 0.0
+    for x in ("a", "b"):
+        y = O.OTHER[x]
+        exp = ins_left(col_left(C[(x, 1)], T[(x, 1)], T[(y, 1)], C[(y, 4)]), T[(x, 2)], S[x], S[y], T[(y, 4)])
+        got = col_left(nC[(y, 1)], nT[(y, 1)], nT[(x, 1)], nC[(x, 4)])
+        worst = max(worst, min(np.abs(_nrm(got) - _nrm(exp)).max(), np.abs(_nrm(got) + _nrm(exp)).max()))
+    assert worst > 1e-3, worst
