@@ -36,6 +36,23 @@ import ctm_inputs as ci  # noqa: E402
 
 FP64_PEAK_TFLOPS = 37.14   # measured DMMA.8x8x4 loop peak on this pool's B200 (profiles/r01_probe_fp64.txt)
 FP64_DFMA_PEAK_TFLOPS = 36.93   # measured DFMA loop peak, same file
+
+
+def hbm_peak_gbs():
+    """Measured copy bandwidth (MEASURED_PEAKS.json hbm_gbs; driver-written)."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        return None
+
+
+def renv_flops(cfg):
+    """Algorithmic flops of one reduced environment with injected side isometries (rows a1,
+    a3, a4 and the v^1 Q GEMMs of a2; SURVEY 8(a) closed form, chi = chi' = chi''):
+    F_chain + 12 chi^3 D^2 + 4 chi^3 D (2 Q products, 2 v^1 Q, the T'^2 chain, C', C'', C' T', (C' T') C'')."""
+    c, D, d = float(cfg.chi), float(cfg.D), float(cfg.d)
+    chain = 4 * c ** 3 * D ** 3 + 4 * d * c ** 3 * D ** 3 + 4 * d * c ** 2 * D ** 5
+    return chain + 12 * c ** 3 * D ** 2 + 4 * c ** 3 * D
 METRIC = "CTM moves/sec and FP64 TFLOP/s (% of B200 FP64 peak) vs D,chi"
 
 
@@ -260,6 +277,29 @@ def bench_ours(args, cfg):
         pfull = []
         for _ in range(3):
             step(inject=False, handle=hp, stats=pfull)
+        # rows a1, a3, a4 timed alone: the reduced environment of each cut type with its side
+        # isometries injected (no SVD) -- half of the method's flops, otherwise only measured
+        # inside the isometry stage on the worker streams
+        renv = {}
+        for x, X in (("a", A), ("b", B)):
+            M = torch.empty(cfg.chi * cfg.D * cfg.D * cfg.chi, dtype=torch.float64, device=dev)
+            n1 = min(cfg.chi_pp, cfg.chi * cfg.D)
+            n2 = min(cfg.chi_pp, n1 * cfg.D)
+            side = torch.empty(2 * (cfg.chi * cfg.D * n1 + n1 * cfg.D * n2), dtype=torch.float64, device=dev)
+            args = (env.C[(x, 1)], env.T[(x, 2)], env.C[(x, 2)], env.T[(x, 1)], X, X, env.T[(x, 3)], M)
+            h.ctm_reduced_env(*args, iso_out=side)
+            renv[x] = (args, side)
+        ms_r = []
+        for i in range(2 + 2 * args.steps):
+            x = "ab"[i % 2]
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record(stream)
+            h.ctm_reduced_env(*renv[x][0], iso_in=renv[x][1])
+            e1.record(stream)
+            e1.synchronize()
+            if i >= 2:
+                ms_r.append(e0.elapsed_time(e1))
         # end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
         pinned = {"A": torch.from_numpy(g["A"]).pin_memory(), "B": torch.from_numpy(g["B"]).pin_memory()}
         hC = {k: torch.from_numpy(v.reshape(-1)).pin_memory() for k, v in g["C"].items()}
@@ -305,10 +345,13 @@ def bench_ours(args, cfg):
     full_n = float(np.mean([s["gemm_launches"] for s in pfull]))
     full_achieved = full_fl / (full_ms * 1e-3) / 1e12
     jac_ms = float(np.mean([s["ms_jacobi"] for s in stats]))
-    jac_fl = float(np.mean([s["jacobi_flops"] for s in stats]))
     jac_n = float(np.mean([s["n_jacobi"] for s in stats]))
-    jac_achieved = jac_fl / (jac_ms * 1e-3) / 1e12 if jac_ms > 0 else None
-    jac_sms = float(np.mean([s["jacobi_cta_ms"] for s in stats])) / jac_ms if jac_ms > 0 else None
+    t_renv = float(np.mean(ms_r))
+    F_renv = renv_flops(cfg)
+    k7_ms = float(np.mean([s["ms_commit"] for s in pst]))
+    k7_bytes = float(np.mean([s["commit_bytes"] for s in pst]))
+    k7_n = float(np.mean([s["n_commit"] for s in pst]))
+    hbm = hbm_peak_gbs()
     if rank != 0:
         return
     value = job_value(world, t_step)
@@ -334,28 +377,37 @@ def bench_ours(args, cfg):
 
         "flops_per_move": F_move,
         "tflops_full_move": F_move / (t_step * 1e-3) / 1e12,
-        # the dominant kernel family of the step by device time (profiles/r01_final_ncu_launches_bench_step.txt:
-        # tc_gemm 34%, Jacobi 26%, Cholesky 25%): tc_gemm over every launch of the full step -- the absorption's
-        # contraction chains and the isometry solvers' small GEMMs -- timed by CUDA events on each launch's stream
-        "roofline": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4), all launches of the full step",
-                     "achieved": full_achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": full_achieved / FP64_PEAK_TFLOPS, "traffic": None,
-                     "launches_per_step": full_n, "ms_per_step": full_ms, "flops_per_step": full_fl,
-                     "note": "the solver GEMMs are 1024 x 160-class, latency bound (split-K); the contraction "
-                             "launches alone: roofline_contraction",
+        # headline roofline: the method's algorithmic flops per step (SURVEY 8(a) closed form F_move, rows
+        # a1-a11; the isometry solver's own GEMMs are NOT counted) over the device time of the whole step
+        "roofline": {"bound": "tensor", "kernel": "whole left move (rows a1-a11: reduced envs, isometry solves, "
+                                                  "chains, corners, commit)",
+                     "achieved": F_move / (t_step * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": F_move / (t_step * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,
+                     "flops_per_step": F_move, "ms_per_step": t_step,
                      "peak_source": "measured DMMA loop (profiles/r01_probe_fp64.txt); MEASURED_PEAKS.json has no FP64"},
-        # the ISO solver's one-sided Jacobi SVD, FP64 on the CUDA cores, latency/issue-bound on 1-8 CTAs
-        # per launch; timed by CUDA events on the worker streams
-        "roofline_jacobi": ({"bound": "alu", "kernel": "jacobi_cluster_kernel (one-sided Jacobi, FP64 DFMA)",
-                      "achieved": jac_achieved, "peak": FP64_DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                      "frac": jac_achieved / FP64_DFMA_PEAK_TFLOPS, "traffic": None,
-                      "launches_per_step": jac_n, "ms_per_step": jac_ms, "flops_per_step": jac_fl,
-                      "flops_unit": "6 n^2 (n-1) per executed sweep",
-                      "sms_occupied_avg": jac_sms,
-                      "frac_of_occupied_sms": jac_achieved / (FP64_DFMA_PEAK_TFLOPS / 148 * jac_sms),
-                      "peak_source": "measured DFMA loop, whole GPU (profiles/r01_probe_fp64.txt); one launch "
-                                     "occupies 1-8 SMs, whose share of that peak is 1-8 x 0.25 TFLOP/s"}
-                     if jac_achieved else None),
+        # rows a1, a3, a4 alone (side isometries injected): the other half of the method's flops
+        "roofline_renv": {"bound": "tensor", "kernel": "tc_gemm, one reduced environment (rows a1, a3, a4 + v1^T Q), "
+                                                       "side isometries injected",
+                          "achieved": F_renv / (t_renv * 1e-3) / 1e12, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                          "frac": F_renv / (t_renv * 1e-3) / 1e12 / FP64_PEAK_TFLOPS, "traffic": None,
+                          "flops_per_call": F_renv, "ms_per_call": t_renv, "calls_per_move": 4,
+                          "note": "CUDA events around ctm_reduced_env(iso_in) on the library stream, L2 flushed"},
+        # K7: Frobenius normalise + commit of the six new tensors, HBM-bound
+        "roofline_commit": ({"bound": "hbm", "kernel": "scale_commit_kernel (K7)",
+                             "achieved": k7_bytes / (k7_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                             "frac": (k7_bytes / (k7_ms * 1e-3) / 1e9 / hbm) if hbm else None, "traffic": None,
+                             "bytes_per_step": k7_bytes, "ms_per_step": k7_ms, "launches_per_step": k7_n,
+                             "peak_source": "MEASURED_PEAKS.json hbm_gbs"} if k7_ms > 0 else None),
+        # the isometry solver (rows a2, a5 SVDs) is reported in ms, not as a flop rate
+        "solver": {"ms_isometry_stage_per_move": ms_iso, "ms_svd_calls_summed_per_move": ms_svd,
+                   "ms_jacobi_summed_per_move": jac_ms, "jacobi_launches_per_move": jac_n,
+                   "solver_and_contraction_gemm_ms_summed": full_ms, "gemm_flops_summed": full_fl,
+                   "gemm_launches": full_n,
+                   "note": "isometry stage = wall time of rows a1-a5 (fork to join); solver GEMM flops are not the "
+                           "method's flops"},
+        "truncation_gaps": {"main_cut_gap[absorption][ab,ba]": stats[0]["cut_gap"],
+                            "side_gap[absorption][a-l,a-r,b-l,b-r]": stats[0]["side_gap"],
+                            "min_gap": float(np.min([s["min_gap"] for s in stats]))},
         "roofline_contraction": {"bound": "tensor", "kernel": "tc_gemm (FP64 DMMA.8x8x4)", "achieved": achieved,
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
                      "traffic": traffic_bytes(cfg), "traffic_unit": "DRAM bytes per step (ncu, profiles/r01_final_traffic.json)",

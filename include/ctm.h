@@ -166,6 +166,11 @@ typedef struct {
                        b-left, b-right (Q_l = C^1 T^1, Q_r = C^2 T^3).             */
   double cut_gap[2][2];
   double side_gap[2][4];
+  /* CTM_FLAG_PROFILE only: the normalise + commit launches (K7, HBM-bound), timed by CUDA
+     events; bytes = algorithmic traffic (read the six new tensors + write them to the env) */
+  double ms_commit;
+  double commit_bytes;
+  int n_commit;
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by
@@ -190,10 +195,12 @@ int ctm_abi_version(void);
  * (v_l1, v_l2) = TS(C^1 T^1; chi'', chi''), (v_r1, v_r2) = TS(C^2 T^3; chi'', chi'').
  * iso_out (nullable) receives vl1, vl2, vr1, vr2 back to back (shapes
  * (chi,D,n1), (n1,D,n2) twice, n1 = min(chi'', chi D), n2 = min(chi'', n1 D)).
- * Synchronises the stream (SVDs). */
+ * iso_in (nullable, APPROX only, same layout): inject the side isometries -- no SVD, only
+ * the contractions of rows a1, a3, a4 (and v^1 Q of a2); asynchronous.
+ * Otherwise synchronises the stream (SVDs). */
 int ctm_reduced_env(ctm_handle h, const double* C1, const double* T2, const double* C2,
                     const double* T1, const double* X, const double* Xbra, const double* T3,
-                    int mode, double* M_out, double* iso_out);
+                    int mode, double* M_out, const double* iso_in, double* iso_out);
 
 /* ctm_ts_isometry: the two-stage isometry TS(Q; c1, c2) of P:L60 ("we reshape it to matrix
  * of dimension chi D x chi D ... take the first chi' left singular vectors as U_d^1 ...

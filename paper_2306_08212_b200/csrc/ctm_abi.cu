@@ -242,6 +242,22 @@ SideOut side_ts(Handle& h, const RenvIn& in, bool left, int chi_pp) {
   return o;
 }
 
+// a1 + the v^1 contraction of a2 with INJECTED side isometries (no SVD): the reduced-env
+// contractions timed alone (bench.py roofline_renv).  v (v1 (P, D, n1), v2 (n1, D, n2)).
+SideOut side_inject(Handle& h, const RenvIn& in, bool left, const double* v1, const double* v2, int n1, int n2) {
+  const int D = in.T1.ext[1];
+  SideOut o;
+  Ten Q = left ? alloc(h, {in.C1.ext[1], D, D, in.T1.ext[0]}) : alloc(h, {in.C2.ext[0], D, D, in.T3.ext[3]});
+  if (left) contract(h, op({&in.C1}, "xp"), op({&in.T1}, "qkbx"), out({&Q}, "pkbq"));
+  else contract(h, op({&in.C2}, "px"), op({&in.T3}, "xkbq"), out({&Q}, "pkbq"));
+  const int P = Q.ext[0], F = Q.ext[3];
+  o.v.v1 = Ten{const_cast<double*>(v1), {P, D, n1}};
+  o.v.v2 = Ten{const_cast<double*>(v2), {n1, D, n2}};
+  o.Q2 = alloc(h, {n1, D, F});
+  contract(h, op({&o.v.v1}, "pka"), op({&Q}, "pkbq"), out({&o.Q2}, "abq"));
+  return o;
+}
+
 // a3 + a4: M = C' T'^2 C'' from the two side isometries.
 RenvOut renv_finish(Handle& h, const RenvIn& in, const SideOut& L, const SideOut& R) {
   RenvOut o;
@@ -664,7 +680,20 @@ void commit_six(Handle& h, ctm_env* env, Ten nT[2], Ten nC1[2], Ten nC4[2], cons
       dst.push_back(env->C[x][3]);
       n.push_back(nC4[x].size());
     }
+    const bool prof = (p.flags & CTM_FLAG_PROFILE) != 0;
+    if (prof) CTM_CUDA(cudaEventRecord(h.ev[6], h.stream));
     scale_commit(h, src, dst, n, ss, nparts);
+    if (prof) {   // K7 (HBM-bound): one launch reads the six new tensors and writes them to the env
+      CTM_CUDA(cudaEventRecord(h.ev[7], h.stream));
+      CTM_CUDA(cudaEventSynchronize(h.ev[7]));
+      float ms = 0.f;
+      CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[6], h.ev[7]));
+      h.ms_commit += ms;
+      size_t tot = 0;
+      for (size_t v : n) tot += v;
+      h.commit_bytes += 2.0 * 8.0 * (double)tot;
+      ++h.n_commit;
+    }
     if (p.flags & CTM_FLAG_CHECK_FINITE) {
       int* cnt = reinterpret_cast<int*>(h.dev_scalars);
       CTM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int), h.stream));
@@ -1118,6 +1147,9 @@ void begin_call(Handle& h) {
   h.prof_ms_subs = 0.0;
   h.prof_flops_subs = 0.0;
   h.prof_n_subs = 0;
+  h.ms_commit = 0.0;
+  h.commit_bytes = 0.0;
+  h.n_commit = 0;
   for (auto& r : h.cut_gap)
     for (double& g : r) g = std::numeric_limits<double>::infinity();
   for (auto& r : h.side_gap)
@@ -1144,6 +1176,9 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->ms_gemm = h.prof_ms_subs;
   st->gemm_flops = h.prof_flops_subs;
   st->gemm_launches = h.prof_used + h.prof_n_subs;
+  st->ms_commit = h.ms_commit;
+  st->commit_bytes = h.commit_bytes;
+  st->n_commit = h.n_commit;
   for (int a = 0; a < 2; ++a) {
     for (int c = 0; c < 2; ++c) st->cut_gap[a][c] = h.cut_gap[a][c];
     for (int i = 0; i < 4; ++i) st->side_gap[a][i] = h.side_gap[a][i];
@@ -1432,10 +1467,11 @@ int ctm_ts_isometry(ctm_handle hh, const double* Q, int P, int K, int Bd, int F,
 
 int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const double* C2, const double* T1,
                     const double* X, const double* Xbra, const double* T3, int mode, double* M_out,
-                    double* iso_out) {
+                    const double* iso_in, double* iso_out) {
   return guarded(hh, [&](Handle& h) {
     if (!C1 || !T2 || !C2 || !T1 || !X || !Xbra || !T3 || !M_out) throw Error(CTM_E_ARG, "null pointer");
     if (mode != CTM_RENV_APPROX && mode != CTM_RENV_EXACT) throw Error(CTM_E_ARG, "unknown reduced-env mode");
+    if (iso_in && mode != CTM_RENV_APPROX) throw Error(CTM_E_ARG, "iso_in needs CTM_RENV_APPROX");
     begin_call(h);
     const ctm_params& p = h.prm;
     const int D = p.D, c = p.chi;
@@ -1452,7 +1488,16 @@ int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const dou
     ctm::RenvIn ri{{const_cast<double*>(C1), {c, c}},       {const_cast<double*>(T2), {c, D, D, c}},
                    {const_cast<double*>(C2), {c, c}},       {const_cast<double*>(T1), {c, D, D, c}},
                    {const_cast<double*>(T3), {c, D, D, c}}, &st};
-    ctm::RenvOut ro = ctm::reduced_env(h, ri, p.chi_pp);
+    ctm::RenvOut ro;
+    if (iso_in) {   // injected side isometries: the contractions of rows a1, a3, a4 only
+      const int n1 = std::min(p.chi_pp, c * D), n2 = std::min(p.chi_pp, n1 * D);
+      const size_t s1 = (size_t)c * D * n1, s2 = (size_t)n1 * D * n2;
+      ctm::SideOut L = ctm::side_inject(h, ri, true, iso_in, iso_in + s1, n1, n2);
+      ctm::SideOut R = ctm::side_inject(h, ri, false, iso_in + s1 + s2, iso_in + 2 * s1 + s2, n1, n2);
+      ro = ctm::renv_finish(h, ri, L, R);
+    } else {
+      ro = ctm::reduced_env(h, ri, p.chi_pp);
+    }
     CTM_CUDA(cudaMemcpyAsync(M_out, ro.M.p, ro.M.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
     if (iso_out) {
       double* o = iso_out;
@@ -1461,7 +1506,7 @@ int ctm_reduced_env(ctm_handle hh, const double* C1, const double* T2, const dou
         o += t->size();
       }
     }
-    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    if (!iso_in) CTM_CUDA(cudaStreamSynchronize(h.stream));   // (injected: no SVD, asynchronous)
   });
 }
 

@@ -71,7 +71,7 @@ struct Handle {
   std::vector<char> host_buf;          // cuSOLVER host workspace
   int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
   double* dev_scalars = nullptr;        // small device scratch (norms etc.)
-  cudaEvent_t ev[8]{};   // 2,3: svd timing; 4,5: isometry fork/join; 6,7: iso solver debug
+  cudaEvent_t ev[8]{};   // 2,3: svd timing; 4,5: isometry fork/join; 6,7: iso solver debug / K7 profile
   cudaEvent_t jev[2]{};  // ISO solver: the pending Jacobi launch (ms_jacobi)
   std::string last_error;
   int64_t kernel_count = 0;
@@ -92,6 +92,8 @@ struct Handle {
   double cut_gap[2][2] = {{1e300, 1e300}, {1e300, 1e300}};
   double side_gap[2][4] = {{1e300, 1e300, 1e300, 1e300}, {1e300, 1e300, 1e300, 1e300}};
   int device = 0;                       // CUDA device the handle (and its workers) run on
+  double ms_commit = 0.0, commit_bytes = 0.0;   // CTM_FLAG_PROFILE: K7 normalise + commit launches
+  int n_commit = 0;
   bool dry = false;                     // sizing pass: no launches
   // CTM_FLAG_PROFILE: event pairs around each tc_gemm launch
   std::vector<cudaEvent_t> prof_ev;

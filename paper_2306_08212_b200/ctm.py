@@ -53,7 +53,8 @@ class ctm_move_stats(ctypes.Structure):
                 ("gemm_flops", c_double), ("gemm_launches", c_int), ("ms_isometry", c_double),
                 ("n_svd_fallback", c_int), ("ms_jacobi", c_double), ("jacobi_flops", c_double),
                 ("n_jacobi", c_int), ("jacobi_cta_ms", c_double),
-                ("cut_gap", (c_double * 2) * 2), ("side_gap", (c_double * 4) * 2)]
+                ("cut_gap", (c_double * 2) * 2), ("side_gap", (c_double * 4) * 2),
+                ("ms_commit", c_double), ("commit_bytes", c_double), ("n_commit", c_int)]
 
     def as_dict(self):
         out = {}
@@ -81,7 +82,7 @@ def lib():
             "ctm_set_stream": (c_int, [P, c_uint64]),
             "ctm_destroy": (c_int, [P]),
             "ctm_last_error": (ctypes.c_char_p, [P]),
-            "ctm_reduced_env": (c_int, [P, P, P, P, P, P, P, P, c_int, P, P]),
+            "ctm_reduced_env": (c_int, [P, P, P, P, P, P, P, P, c_int, P, P, P]),
             "ctm_absorb_truncate": (c_int, [P, P, P, P, P, P, P, P, P]),
             "ctm_left_move": (c_int, [P, P, P, POINTER(ctm_env), P, P, POINTER(ctm_move_stats)]),
             "ctm_move": (c_int, [P, c_int, P, P, POINTER(ctm_env), P, POINTER(ctm_move_stats)]),
@@ -173,9 +174,9 @@ class CtmHandle:
                                               _ptr(v1_out), _ptr(v2_out), _ptr(T_out)))
         return T_out
 
-    def ctm_reduced_env(self, C1, T2, C2, T1, X, Xbra, T3, M_out, iso_out=None, mode=CTM_RENV_APPROX):
+    def ctm_reduced_env(self, C1, T2, C2, T1, X, Xbra, T3, M_out, iso_out=None, mode=CTM_RENV_APPROX, iso_in=None):
         self._check(lib().ctm_reduced_env(self.h, _ptr(C1), _ptr(T2), _ptr(C2), _ptr(T1), _ptr(X), _ptr(Xbra),
-                                          _ptr(T3), mode, _ptr(M_out), _ptr(iso_out)))
+                                          _ptr(T3), mode, _ptr(M_out), _ptr(iso_in), _ptr(iso_out)))
         return M_out
 
     def ctm_left_move(self, A, B, env, iso_in=None, iso_out=None, stats=True):

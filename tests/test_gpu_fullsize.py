@@ -224,3 +224,23 @@ def test_shadowed_trajectory(name, n_iter):
         print(f"{name} iteration {it + 1}: worst projector err/bar {w:.3f}, injected-entrywise "
               f"{max(r[2] for r in log[-4:]):.2e}, own-move column {max(r[3] for r in log[-4:]):.2e}, "
               f"e_H {e_gpu:.10f}")
+
+
+@pytest.mark.parametrize("name", ["c2", "c4"])
+def test_reduced_env_with_injected_side_isometries(name):
+    """ctm_reduced_env(iso_in): the contractions of rows a1, a3, a4 with the side isometries
+    injected (the bench's roofline_renv path) reproduce the full call's M exactly."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    C, T, A = g["C"], g["T"], g["A"]
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_MOVE_ONLY)
+    n1 = min(cfg.chi_pp, cfg.chi * cfg.D)
+    n2 = min(cfg.chi_pp, n1 * cfg.D)
+    side = torch.zeros(2 * (cfg.chi * cfg.D * n1 + n1 * cfg.D * n2), dtype=torch.float64, device=DEV)
+    args = [T_(C[("a", 1)]), T_(T[("a", 2)]), T_(C[("a", 2)]), T_(T[("a", 1)]), T_(A), T_(A), T_(T[("a", 3)])]
+    M1 = torch.empty((cfg.chi, cfg.D, cfg.D, cfg.chi), dtype=torch.float64, device=DEV)
+    M2 = torch.empty_like(M1)
+    h.ctm_reduced_env(*args, M1, iso_out=side)
+    h.ctm_reduced_env(*args, M2, iso_in=side)
+    torch.cuda.synchronize()
+    assert rel_err(M2.cpu().numpy(), M1.cpu().numpy()) <= 1e-14

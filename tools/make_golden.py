@@ -42,8 +42,32 @@ def run(name, n_left_moves=None, n_iter=None):
     return out
 
 
+def run_dl(name, n_iter):
+    """Gauge-invariant values after each of n_iter CTM iterations of a converging (R16b)
+    config -- the GPU test compares its own trajectory at 1e-9 (the oracle's
+    perturbed-start spread stays ~1e-14 on c4_dl, profiles/r02_spread_c4_dl.txt)."""
+    cfg = ci.CONFIGS[name]
+    g = ci.generate(cfg)
+    env = {"C": g["C"], "T": g["T"]}
+    A, B = g["A"], g["B"]
+    out = {"config": name, "seed": cfg.seed, "d": cfg.d, "D": cfg.D, "chi": cfg.chi, "iterations": []}
+    t = time.time()
+    for it in range(n_iter):
+        env = O.ctm_iteration(env, A, B, cfg.chi, cfg.chi_p, cfg.chi_pp)
+        out["iterations"].append(observables(env, A, B))
+        print(name, it + 1, out["iterations"][-1], round(time.time() - t, 1), flush=True)
+    out["oracle_seconds"] = time.time() - t
+    return out
+
+
 if __name__ == "__main__":
     gold = os.path.join(ROOT, "tests", "golden")
+    if "--dl" in sys.argv:   # the converging c4_dl trajectory (slow: ~15 min on 8 cores)
+        res = {"_source": "written by tools/make_golden.py --dl from oracle/ only (no CUDA path)",
+               "c4_dl": run_dl("c4_dl", 20)}
+        with open(os.path.join(gold, "oracle_c4_dl.json"), "w") as f:
+            json.dump(res, f, indent=1)
+        sys.exit(0)
     res = {"_source": "written by tools/make_golden.py from oracle/ only (no CUDA path)",
            "tiny": run("tiny", n_left_moves=1, n_iter=1),
            "c2": run("c2", n_left_moves=1, n_iter=20)}
