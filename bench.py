@@ -286,9 +286,9 @@ def bench_ours(args, cfg):
             n1 = min(cfg.chi_pp, cfg.chi * cfg.D)
             n2 = min(cfg.chi_pp, n1 * cfg.D)
             side = torch.empty(2 * (cfg.chi * cfg.D * n1 + n1 * cfg.D * n2), dtype=torch.float64, device=dev)
-            args = (env.C[(x, 1)], env.T[(x, 2)], env.C[(x, 2)], env.T[(x, 1)], X, X, env.T[(x, 3)], M)
-            h.ctm_reduced_env(*args, iso_out=side)
-            renv[x] = (args, side)
+            rargs = (env.C[(x, 1)], env.T[(x, 2)], env.C[(x, 2)], env.T[(x, 1)], X, X, env.T[(x, 3)], M)
+            h.ctm_reduced_env(*rargs, iso_out=side)
+            renv[x] = (rargs, side)
         ms_r = []
         for i in range(2 + 2 * args.steps):
             x = "ab"[i % 2]

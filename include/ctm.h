@@ -92,10 +92,10 @@ extern "C" {
 #define CTM_RENV_EXACT 1     /* exact Fig 3(b) network, P:L53 (NEXT on GPU)            */
 
 /* two-stage isometry modes (ctm_ts_isometry) */
-#define CTM_TS_MAIN 0        /* both stages are SVDs (left singular vectors, sign rule)     */
-#define CTM_TS_SIDE 1        /* a stage two that truncates nothing returns an orthonormal
-                                basis of its column space (reading R24: the side isometries
-                                only build M, where that basis cancels)                     */
+#define CTM_TS_SVD 0         /* both stages are SVDs (left singular vectors, sign rule)     */
+#define CTM_TS_BASIS 1       /* what ctm_left_move runs for every cut: a stage two that
+                                truncates nothing returns an orthonormal basis of its column
+                                space (same projector v v^T; readings R24 side, R24b main)  */
 
 /* bonds (ctm_bond_energy) */
 #define CTM_BOND_H 0         /* A left of B: 2x1 window                               */
@@ -213,7 +213,7 @@ int ctm_reduced_env(ctm_handle h, const double* C1, const double* T2, const doub
  *              Q2 = v1^T Q as (n1 B) x F;   c2 <= chi.
  *   v1_out, v2_out: device, caller-owned.  gaps_host (nullable, 2 doubles): the stage gaps
  *   sigma_n / sigma_{n+1} (+inf where nothing is truncated).
- *   mode CTM_TS_MAIN / CTM_TS_SIDE (above).  Synchronises the stream.  The same routine the
+ *   mode CTM_TS_SVD / CTM_TS_BASIS (above).  Synchronises the stream.  The same routine the
  *   move runs for every cut (the a5 parity tests call it on a given M). */
 int ctm_ts_isometry(ctm_handle h, const double* Q, int P, int K, int B, int F, int c1, int c2, int mode,
                     double* v1_out, double* v2_out, double* gaps_host);

@@ -191,10 +191,13 @@ std::vector<int> chains(Handle& h, const std::vector<ChainJob>& jobs) {
 //   Q (P, D, D, F) as (boundary, ket, bra, far); returns v1 (P, D, n1), v2 (n1, D, n2) and
 //   optionally Q2 = v1^T Q (n1, D, F), which the reduced env reuses for C' (row a4).
 // ---------------------------------------------------------------------------------------
-// side: the isometries only build the reduced environment M = C' T'^2 C'' (rows a3, a4),
-// where the stage-two output bond is contracted on both sides, so a non-truncating stage
-// two may return any orthonormal basis (reading R24): svd_left's basis_only.
-Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool side = false) {
+// basis2: a stage two that truncates nothing ((n1 D) x F keeping all F columns) returns an
+// orthonormal basis of its column space instead of its left singular vectors (svd_left's
+// basis_only; readings R24, R24b): the projector v v^T -- all the move uses -- is the same.
+// The move takes it for every cut: side TS (R24: the output bond is contracted on both
+// sides of M) and main TS (R24b: an orthogonal change of the new bond's basis is a gauge
+// transformation of the new environment).
+Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool basis2 = false) {
   const int P = Qt.ext[0], K = Qt.ext[1], Bd = Qt.ext[2], F = Qt.ext[3];
   const int n1 = std::min(c1, P * K);
   Iso r;
@@ -204,7 +207,7 @@ Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool sid
   contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
   const int n2 = std::min(c2, n1 * Bd);
   r.v2 = alloc(h, {n1, Bd, n2});
-  r.gap2 = svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p, side);
+  r.gap2 = svd_left(h, Q2.p, n1 * Bd, F, n2, r.v2.p, basis2);
   if (Q2_keep) *Q2_keep = Q2;
   return r;
 }
@@ -434,7 +437,8 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
       CTM_CUDA(cudaStreamWaitEvent(s.stream, r.ev[0], 0));
     }
     RenvOut ro = renv_finish(s, ri[x], side[2 * x], side[2 * x + 1]);
-    V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr);   // a5
+    static const bool main_svd2 = std::getenv("CTM_TS_MAIN_SVD") != nullptr;   // A/B: SVD stage two
+    V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr, !main_svd2);   // a5 (basis stage two: R24b)
   };
   std::vector<std::function<void()>> T;
   for (int x = 0; x < 2; ++x) {
@@ -1446,7 +1450,7 @@ int ctm_ts_isometry(ctm_handle hh, const double* Q, int P, int K, int Bd, int F,
                     double* v1_out, double* v2_out, double* gaps_host) {
   return guarded(hh, [&](Handle& h) {
     if (!Q || !v1_out || !v2_out) throw Error(CTM_E_ARG, "null pointer");
-    if (mode != CTM_TS_MAIN && mode != CTM_TS_SIDE) throw Error(CTM_E_ARG, "unknown TS mode");
+    if (mode != CTM_TS_SVD && mode != CTM_TS_BASIS) throw Error(CTM_E_ARG, "unknown TS mode");
     const ctm_params& p = h.prm;
     // the workspace is sized for the TS calls of a move: Q up to (chi, D, D, chi)
     if (P < 1 || F < 1 || c1 < 1 || c2 < 1 || P > p.chi || F > p.chi || K != p.D || Bd != p.D ||
@@ -1454,7 +1458,7 @@ int ctm_ts_isometry(ctm_handle hh, const double* Q, int P, int K, int Bd, int F,
       throw Error(CTM_E_ARG, "TS shape outside the handle's (chi, D, D, chi) / chi', chi'' sizing");
     begin_call(h);
     ctm::Ten Qt{const_cast<double*>(Q), {P, K, Bd, F}};
-    ctm::Iso v = ctm::ts_isometry(h, Qt, c1, c2, nullptr, mode == CTM_TS_SIDE);
+    ctm::Iso v = ctm::ts_isometry(h, Qt, c1, c2, nullptr, mode == CTM_TS_BASIS);
     CTM_CUDA(cudaMemcpyAsync(v1_out, v.v1.p, v.v1.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
     CTM_CUDA(cudaMemcpyAsync(v2_out, v.v2.p, v.v2.size() * 8, cudaMemcpyDeviceToDevice, h.stream));
     CTM_CUDA(cudaStreamSynchronize(h.stream));

@@ -25,7 +25,7 @@ CTM_FLAG_MOVE_ONLY = 2
 CTM_FLAG_PROFILE = 4
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
-CTM_TS_MAIN, CTM_TS_SIDE = 0, 1
+CTM_TS_SVD, CTM_TS_BASIS = 0, 1
 DIRS = {"left": 0, "right": 1, "up": 2, "down": 3}
 CTM_E_ARG, CTM_E_CUDA, CTM_E_SOLVER, CTM_E_NONFINITE, CTM_E_NOMEM, CTM_E_UNSUPPORTED = 1, 2, 3, 4, 5, 6
 STATUS = {0: "CTM_OK", 1: "CTM_E_ARG", 2: "CTM_E_CUDA", 3: "CTM_E_SOLVER", 4: "CTM_E_NONFINITE",
@@ -193,7 +193,7 @@ class CtmHandle:
                                    byref(st)))
         return st.as_dict()
 
-    def ctm_ts_isometry(self, Q, c1, c2, mode=CTM_TS_MAIN):
+    def ctm_ts_isometry(self, Q, c1, c2, mode=CTM_TS_BASIS):
         """TS(Q; c1, c2) on a (P, K, B, F) device tensor -> (v1, v2, (gap1, gap2))."""
         P_, K, B, F = Q.shape
         n1 = min(c1, P_ * K)
