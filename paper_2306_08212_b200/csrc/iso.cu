@@ -279,7 +279,6 @@ void iso_init_kernels() {   // per device, once (see tc_init_kernels)
   CTM_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
   if (done.count(dev)) return;
-  const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
   set_smem((const void*)chol_kernel, chol_smem_bytes(LMAX));
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
@@ -364,7 +363,15 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     h.ws.reset(mark);
     return gap;
   }
-  // truncating cut: Chebyshev-filtered subspace iteration with Rayleigh-Ritz
+  // truncating cut: Chebyshev-filtered subspace iteration with Rayleigh-Ritz and locking.
+  // Ritz vectors that pass the certificate are LOCKED (moved out of the iterated block): the
+  // active block is kept orthogonal to them, so its dynamic range is that of the unconverged
+  // part of the spectrum.  Without locking, a steep M (sigma_1 / sigma_k >~ 1/sqrt(eps) --
+  // converged physical environments, C3 from the third CTM iteration on) carries its small
+  // kept directions next to sigma_1^2-amplified ones, which rounding swamps: the solve
+  // stalled at residual O(1) and fell back to gesvdp (profiles/r02_c3_fallbacks_before_locking.txt).
+  // With the large directions removed, each product M (M^T y) of an active vector has rounding
+  // error ~ eps sigma_1 sigma_i: the M-form floor of the certificate, as for LAPACK.
   const int l = std::min(n_keep + iso_oversample(n_keep), R);
   const int k = n_keep;
   double* Y = h.ws.take((size_t)R * l);
@@ -378,13 +385,18 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   double* U = h.ws.take((size_t)R * l);
   double* PW = h.ws.take((size_t)R * l);
   double* res = h.ws.take((size_t)l);
+  double* L = h.ws.take((size_t)R * l);    // locked Ritz vectors, R x nlock contiguous
+  double* Lt = h.ws.take((size_t)R * l);   // rebuild scratch / final assembly
+  double* Tp = h.ws.take((size_t)l * l);   // L^T Y
   ++h.n_svd;
   static const bool debug = std::getenv("CTM_ISO_DEBUG") != nullptr;
   cudaEvent_t t0 = h.ev[2];
   float ms_rr = 0.f, ms_all = 0.f;
-  auto GY = [&](const double* X, double* out) {   // out = M M^T X; leaves M^T X in Z
-    sv.gemm(mat, "ic", {R, C}, X, "ia", {R, l}, Z, "ca", {C, l});
-    sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, out, "ia", {R, l});
+  int la = l, nlock = 0;                   // active columns, locked columns
+  std::vector<double> s_lock;
+  auto GY = [&](const double* X, double* out) {   // out = M M^T X; leaves M^T X in Z (la columns)
+    sv.gemm(mat, "ic", {R, C}, X, "ia", {R, la}, Z, "ca", {C, la});
+    sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, la}, out, "ia", {R, la});
   };
   // Filter products through G = M M^T (one GEMM per degree instead of two) when the
   // kept spectrum is flat: the containment floor of the G-form is ~ eps (s_1/s_k)^2,
@@ -392,16 +404,29 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   double* G = h.ws.take((size_t)R * R);
   bool have_G = false;
   auto GYf = [&](const double* X, double* out) {
-    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, l}, out, "ia", {R, l});
+    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, la}, out, "ia", {R, la});
     else GY(X, out);
   };
   auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c) {
     if (h.dry) return;
-    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, Pm, Yc, Yo, (long long)R * l, a, b2, c);
+    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, Pm, Yc, Yo, (long long)R * la, a, b2, c);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   };
-  // start: Y = orth(M Omega), then two plain steps Y <- orth(M M^T Y)
+  // X <- X - L (L^T X): remove the locked directions from an active iterate (scratch: R x la)
+  auto project = [&](double* X, double* scratch) {
+    if (nlock == 0) return;
+    sv.gemm(L, "ij", {R, nlock}, X, "ia", {R, la}, Tp, "ja", {nlock, la});
+    sv.gemm(L, "ij", {R, nlock}, Tp, "ja", {nlock, la}, scratch, "ia", {R, la});
+    combine(X, scratch, X, nullptr, -1.0, 1.0, 0.0);
+  };
+  // columns [c0, c0 + nc) of a row-major R x ld matrix into a contiguous R x nc one
+  auto copy_cols = [&](double* dst, int dld, int d0, const double* src, int sld, int c0, int nc) {
+    if (h.dry || nc == 0) return;
+    CTM_CUDA(cudaMemcpy2DAsync(dst + d0, sizeof(double) * dld, src + c0, sizeof(double) * sld, sizeof(double) * nc, R,
+                               cudaMemcpyDeviceToDevice, h.stream));
+  };
+  // start: Y = orth(M Omega), then four plain steps Y <- orth(M M^T Y)
   if (!h.dry) {
     launch_k(fill_omega_kernel, dim3(148), dim3(256), 0, h.stream, Z, (long long)C * l, 0x5eed1234u);
     CTM_CUDA(cudaGetLastError());
@@ -415,12 +440,15 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     sv.cholqr(Y, R, l, 1, true, nullptr);
   }
   std::vector<double> s(l), r(k);
-  double prev_worst = inf;
+  double prev_worst = inf, prev_floor = inf;
   int degrees = 4, checks = 0;
   const int max_degrees = 400;
+  const double cert = 8.0 * EPS * std::sqrt((double)C);
+  bool plateau = false;
   for (;;) {
     ++checks;
-    // Rayleigh-Ritz on an orthonormal Y: Z = M^T Y, P = M Z, Z = Q_z R_z, W = lsv(R_z^T)
+    const int ka = k - nlock;   // wanted vectors still active
+    // Rayleigh-Ritz on the orthonormal active block: Z = M^T Y, P = M Z, Z = Q_z R_z, W = lsv(R_z^T)
     cudaEvent_t e_rr0 = h.ev[6], e_rr1 = h.ev[7];
     if (!h.dry && debug) CTM_CUDA(cudaEventRecord(e_rr0, h.stream));
     // orthonormal basis: Y leaves the filter (or the start) through a shifted CholQR, so its
@@ -430,34 +458,47 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // (the first check only estimates the spectrum for the filter bounds: one plain pass on
     // Y and one shifted pass on Z suffice -- C4 57.0 -> 56.2 ms, C5 246 -> 240 ms; no pass on
     // Y at all mis-set the C5 bounds)
+    // with locked vectors: project them out before each pass ("twice is enough")
     const bool light = checks == 1;
-    if (light) sv.cholqr(Y, R, l, 1, false, nullptr, true);
-    else if (l <= LMAX) sv.cholqr(Y, R, l, 2, false, nullptr, true);
-    else sv.cholqr(Y, R, l, 3, true, nullptr, true);
+    if (light) {
+      sv.cholqr(Y, R, la, 1, false, nullptr, true);
+    } else if (nlock > 0 || h.dry) {
+      project(Y, PW);
+      sv.cholqr(Y, R, la, 1, false, nullptr, true);
+      project(Y, PW);
+      sv.cholqr(Y, R, la, 1, false, nullptr, false);
+    } else if (la <= LMAX) {
+      sv.cholqr(Y, R, la, 2, false, nullptr, true);
+    } else {
+      sv.cholqr(Y, R, la, 3, true, nullptr, true);
+    }
     GY(Y, P);
-    sv.cholqr(Z, C, l, light ? 1 : 2, true, Rz);   // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR2)
+    sv.cholqr(Z, C, la, light ? 1 : 2, true, Rz);   // Z = M^T Y (left in Z by GY) = Q_z R_z (sCholQR2)
     // the first Rayleigh-Ritz only seeds the filter bounds: a capped, loose Jacobi suffices
     // (one sweep: C4 74.5 -> 71 ms vs three; zero sweeps -- column norms only -- mis-set the
     // C5 filter bounds and cost a fallback)
-    if (checks == 1) sv.jacobi(Rz, l, 1, l, W, S, 1e-6, 1);
-    else sv.jacobi(Rz, l, 1, l, W, S, 1e-14);
-    sv.gemm(Y, "ia", {R, l}, W, "ab", {l, l}, U, "ib", {R, l});
-    sv.gemm(P, "ia", {R, l}, W, "ab", {l, l}, PW, "ib", {R, l});
-    if (h.dry) {   // sizing pass: also reserve the G-form GEMMs' split-K slabs
+    if (checks == 1) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, 1);
+    else sv.jacobi(Rz, la, 1, la, W, S, 1e-14);
+    sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
+    sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
+    if (h.dry) {   // sizing pass: also reserve the G-form GEMMs' split-K slabs and the projection
       sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
       sv.gemm(G, "ij", {R, R}, Y, "ja", {R, l}, P, "ia", {R, l});
+      nlock = l;
+      project(Y, PW);
       h.ws.reset(mark);
       return inf;
     }
-    launch_k(ritz_residual_kernel, dim3(k), dim3(256), 0, h.stream, (const double*)PW, (const double*)U, (const double*)S,
-             R, l, k, res);
+    launch_k(ritz_residual_kernel, dim3(ka), dim3(256), 0, h.stream, (const double*)PW, (const double*)U, (const double*)S,
+             R, la, ka, res);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
     if (debug) CTM_CUDA(cudaEventRecord(e_rr1, h.stream));
     sv.check_status("iso subspace");
-    if (debug) std::fprintf(stderr, "[iso]   check %d after %d degrees: jacobi sweeps %d\n", checks, degrees, sv.last_sweeps);
-    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * l, cudaMemcpyDeviceToHost, h.stream));
-    CTM_CUDA(cudaMemcpyAsync(r.data(), res, sizeof(double) * k, cudaMemcpyDeviceToHost, h.stream));
+    if (debug) std::fprintf(stderr, "[iso]   check %d after %d degrees: active %d locked %d jacobi sweeps %d\n", checks,
+                            degrees, la, nlock, sv.last_sweeps);
+    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * la, cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaMemcpyAsync(r.data(), res, sizeof(double) * ka, cudaMemcpyDeviceToHost, h.stream));
     CTM_CUDA(cudaStreamSynchronize(h.stream));
     if (debug) {
       float ms = 0.f;
@@ -466,35 +507,66 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     }
     // r_i = ||M (M^T u_i) - s_i^2 u_i||: its rounding floor is ~ eps sqrt(C) s_1 s_i (the
     // product is formed through M, never through a Gram), and r_i / s_i^2 estimates how much
-    // of the true u_i lies outside span(Y).  Accept only when every kept vector's residual
-    // is at that floor (a measured certificate, no extrapolation).
+    // of the true u_i lies outside span(Y).  A vector is certified when its residual is at
+    // that floor (a measured certificate, no extrapolation); the leading certified active
+    // vectors are locked, and the solve ends when every wanted vector is certified.
+    const double s1 = nlock > 0 ? s_lock[0] : s[0];
+    int j = 0;
     double worst = 0.0, worst_floor = 0.0;
-    for (int i = 0; i < k; ++i) {
+    for (int i = 0; i < ka; ++i) {
       if (!std::isfinite(r[i]) || !std::isfinite(s[i]))
         throw Error(CTM_E_NONFINITE, "non-finite Ritz value in a " + std::to_string(R) + " x " + std::to_string(C) +
                                          " isometry");
+      const double f = s[i] > 0.0 ? r[i] / (s1 * s[i]) : 0.0;
+      if (!light && j == i && f <= cert) {
+        ++j;   // leading certified
+        continue;
+      }
       worst = std::max(worst, s[i] > 0.0 ? r[i] / (s[i] * s[i]) : 0.0);
-      worst_floor = std::max(worst_floor, s[i] > 0.0 ? r[i] / (s[0] * s[i]) : 0.0);
+      worst_floor = std::max(worst_floor, f);
     }
-    const bool cert = checks > 1 || k == 0;   // the first Rayleigh-Ritz is an estimate only
     if (debug)
-      std::fprintf(stderr, "[iso]     residual/s_i^2 %.3e  residual/(s_1 s_i) %.3e (cert at %.3e)\n", worst, worst_floor,
-                   8.0 * EPS * std::sqrt((double)C));
-    if (cert && worst_floor <= 8.0 * EPS * std::sqrt((double)C)) break;
+      std::fprintf(stderr, "[iso]     certified %d of %d active wanted; unconverged: residual/s_i^2 %.3e  "
+                           "residual/(s_1 s_i) %.3e (cert at %.3e)\n", j, ka, worst, worst_floor, cert);
+    if (!light && j == ka) break;
+    // a plateau at the rounding floor (no further progress possible in FP64, within 64x of
+    // the nominal floor constant) is accepted: the result is as accurate as the arithmetic
+    if (checks > 2 && worst_floor <= 64.0 * cert && worst_floor > 0.5 * prev_floor) {
+      plateau = true;
+      break;
+    }
     if (degrees >= max_degrees || (checks > 2 && worst > 0.5 * prev_worst))
       throw IsoFail("subspace iteration did not converge: residual " + std::to_string(worst));
     prev_worst = worst;
-    // Chebyshev filter (Zhou & Saad's scaled recurrence) damping [0, b], b = s_l^2 (the
-    // smallest Ritz value of the block), normalised at the k-th Ritz value; the error of
+    prev_floor = worst_floor;
+    // lock the leading certified Ritz vectors: L <- [L, U(:, 0:j)], active <- U(:, j:la)
+    if (j > 0) {
+      copy_cols(Lt, nlock + j, 0, L, nlock, 0, nlock);
+      copy_cols(Lt, nlock + j, nlock, U, la, 0, j);
+      std::swap(L, Lt);
+      for (int i = 0; i < j; ++i) s_lock.push_back(s[i]);
+      copy_cols(Y, la - j, 0, U, la, j, la - j);
+      nlock += j;
+      la -= j;
+      s.erase(s.begin(), s.begin() + j);
+    } else if (checks > 1) {
+      // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
+      // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
+      // (after the capped first check W is not orthogonal: keep filtering Y itself)
+      CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * la, cudaMemcpyDeviceToDevice, h.stream));
+    }
+    const int kb = k - nlock;   // wanted active vectors after locking (>= 1)
+    // Chebyshev filter (Zhou & Saad's scaled recurrence) damping [0, b], b = s_la^2 (the
+    // smallest Ritz value of the active block), normalised at the k-th Ritz value; the error of
     // the slowest kept vector shrinks by x_k + sqrt(x_k^2 - 1) per degree.
-    const double lk = s[k - 1] * s[k - 1], lb = s[l - 1] * s[l - 1], l1 = s[0] * s[0];
-    if (!have_G && l1 <= 16.0 * lk) {   // (256 / 2500: within noise at C4/C5; not worth the floor)
+    const double lk = s[kb - 1] * s[kb - 1], lb = s[la - 1] * s[la - 1], l1 = s[0] * s[0], lg = s1 * s1;
+    if (!have_G && lg <= 16.0 * lk) {   // (256 / 2500: within noise at C4/C5; not worth the floor)
       sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
       have_G = true;
     }
     if (!(lb < 0.999 * lk)) throw IsoFail("no spectral separation inside the block");
     const double ce = 0.5 * lb;                       // centre = half width of [0, b]
-    const double xk = (lk - ce) / ce, x1 = (l1 - ce) / ce;
+    const double xk = (lk - ce) / ce, x1 = (l1 - ce) / ce, xg = (lg - ce) / ce;
     const double rate = xk + std::sqrt(xk * xk - 1.0);
     // the first estimate comes from a young subspace (Ritz values of the block bottom are
     // low, the rate optimistic): over-filter by 1.6x rather than pay another check
@@ -510,59 +582,70 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // <= 0.25 / sqrt(shift): one shifted CholQR pass leaves kappa(Q) ~ sqrt(shift) kappa(Y),
     // so a larger per-block spread compounds from block to block until kept directions
     // drown (seen as Ritz residual blow-ups at l = 288).
-    const double shift_rel = 11.0 * ((double)R * l + (double)l * (l + 1)) * EPS;
+    const double shift_rel = 11.0 * ((double)R * la + (double)la * (la + 1)) * EPS;
     const double spread = std::min(1e6, 0.25 / std::sqrt(shift_rel));
     const double lg_deg = std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12;   // log-spread per degree
-    const int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / lg_deg)));
+    int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / lg_deg)));
     // Longer blocks re-orthonormalised by one PLAIN CholQR pass (no shift: kappa(Q) ~ 1, so
-    // nothing compounds) while the spread stays <= 1e7 (Gram condition 1e14 < 1/eps); the
-    // rounding noise such a block leaves in the kept directions (~ eps * spread) is filtered
-    // away by the last `tail` degrees, which use the short shifted blocks above.
+    // nothing compounds) while the spread stays <= 1e10; the rounding noise such a block leaves
+    // in the kept directions is filtered away by the last `tail` degrees, which use the short
+    // shifted blocks above.
     static const int plain_on = std::getenv("CTM_ISO_PLAIN") ? std::atoi(std::getenv("CTM_ISO_PLAIN")) : 1;
     // (spread 1e7 -> 1e10: columns whose pivot falls below 1e-13 of their norm are re-seeded
     // by the replacement, the shifted tail and the residual certificate guard the result;
     // C5/chi=256 523 -> 400 ms, C5 232 -> 215 ms, no fallbacks; 1e12 within noise of 1e10;
     // a tail of 8 degrees: slower)
-    const int mb_plain = std::max(1, std::min(12, (int)std::floor(std::log(1e10) / lg_deg)));
+    int mb_plain = std::max(1, std::min(12, (int)std::floor(std::log(1e10) / lg_deg)));
+    // locked directions re-enter an active iterate through rounding (~eps) and the filter
+    // amplifies them most (they sit above the active spectrum): project them out at every
+    // orthonormalisation, often enough that they stay below 1e-6 of the active block
+    if (nlock > 0 && xg > x1) {
+      const double lg_lock = std::acosh(xg) - std::acosh(std::max(x1, xk)) + 1e-12;
+      const int mp = std::max(1, (int)std::floor(std::log(1e-6 / EPS) / lg_lock));
+      mb = std::min(mb, mp);
+      mb_plain = std::min(mb_plain, mp);
+    }
     const int tail = 6;
-    // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
-    // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
-    // (after the capped first check W is not orthogonal: keep filtering Y itself)
-    if (checks > 1) CTM_CUDA(cudaMemcpyAsync(Y, U, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
     // One Chebyshev recurrence over all `need` degrees; every mb degrees the current iterate
     // is re-orthonormalised (shifted CholQR, a basis is enough here) and the previous one is
     // multiplied by the same R^{-1}, so the three-term recurrence continues across the
     // orthonormalisation (restarting it at T_1 would give the shifted-power rate x_k per
     // degree instead of x_k + sqrt(x_k^2 - 1) on the steep cuts, where mb = 1: at C5 those
-    // needed a third Rayleigh-Ritz check; C5 move 344 -> 307 ms, C4 +2 ms).
-    const double s1 = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
-    double sig = s1;
+    // needed a third Rayleigh-Ritz check; C5 move 344 -> 307 ms, C4 +2 ms).  The locked
+    // directions are projected out of both iterates (the projector commutes with the
+    // recurrence: span(L) is invariant under M M^T).
+    const double s1c = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
+    double sig = s1c;
     double *Yo = nullptr, *Yc = Y;
     double* bufs[2] = {Y1, Y2};
     int nb = 0, done = 0;
     while (done < need) {
       const bool plain = plain_on && mb_plain > mb && need - done > tail;
       const int m = plain ? std::min(mb_plain, need - done - tail) : std::min(mb, need - done);
-      for (int j = 0; j < m; ++j) {
+      for (int jj = 0; jj < m; ++jj) {
         GYf(Yc, P);
         double* Yn = bufs[nb];
         nb ^= 1;
         if (Yo == nullptr) {
-          combine(Yn, P, Yc, nullptr, s1 / ce, -s1, 0.0);
+          combine(Yn, P, Yc, nullptr, s1c / ce, -s1c, 0.0);
         } else {
-          const double sn = 1.0 / (2.0 / s1 - sig);
+          const double sn = 1.0 / (2.0 / s1c - sig);
           combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn);
           sig = sn;
         }
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
       }
+      if (nlock > 0) {
+        project(Yc, U);
+        project(Yo, U);
+      }
       // (plain blocks replace numerically dependent columns instead of failing: the block's
       // bottom columns -- the oversampling buffer -- can fall below eps of the top ones)
-      sv.cholqr(Yc, R, l, 1, !plain, nullptr, plain, Yo);
+      sv.cholqr(Yc, R, la, 1, !plain, nullptr, plain, Yo);
       done += m;
     }
-    if (!h.dry && Yc != Y) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
+    if (!h.dry && Yc != Y) CTM_CUDA(cudaMemcpyAsync(Y, Yc, sizeof(double) * R * la, cudaMemcpyDeviceToDevice, h.stream));
     degrees += need;
   }
   if (debug) {
@@ -570,11 +653,22 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     CTM_CUDA(cudaEventSynchronize(h.ev[3]));
     CTM_CUDA(cudaEventElapsedTime(&ms_all, t0, h.ev[3]));
   }
-  signfix(h, U, l, 1, R, n_keep, out);
-  if (k < l && s[k] > 0.0) gap = s[k - 1] / s[k];
+  // the kept vectors: the locked ones, then the certified active Ritz vectors
+  const int ka = k - nlock;
+  if (nlock == 0) {
+    signfix(h, U, la, 1, R, n_keep, out);
+  } else {
+    copy_cols(Lt, k, 0, L, nlock, 0, nlock);
+    copy_cols(Lt, k, nlock, U, la, 0, ka);
+    signfix(h, Lt, k, 1, R, n_keep, out);
+  }
+  if (ka < la && s[ka] > 0.0) gap = (ka > 0 ? s[ka - 1] : s_lock.back()) / s[ka];
   if (debug)
-    std::fprintf(stderr, "[iso] %d x %d keep %d: l=%d degrees=%d checks=%d s1/sk=%.3g sl/sk=%.3g gap=%.5f ms=%.2f rr_ms=%.2f last_sweeps=%d\n",
-                 R, C, n_keep, l, degrees, checks, s[0] / s[k - 1], s[l - 1] / s[k - 1], gap, ms_all, ms_rr, sv.last_sweeps);
+    std::fprintf(stderr, "[iso] %d x %d keep %d: l=%d degrees=%d checks=%d locked=%d%s s1/sk=%.3g sl/sk=%.3g gap=%.5f ms=%.2f "
+                         "rr_ms=%.2f last_sweeps=%d\n",
+                 R, C, n_keep, l, degrees, checks, nlock, plateau ? " (plateau)" : "",
+                 (nlock ? s_lock[0] : s[0]) / (ka > 0 ? s[ka - 1] : s_lock.back()), s[la - 1] / (ka > 0 ? s[ka - 1] : s_lock.back()),
+                 gap, ms_all, ms_rr, sv.last_sweeps);
   h.ws.reset(mark);
   return gap;
 }
