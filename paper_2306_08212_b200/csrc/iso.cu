@@ -481,6 +481,11 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     else sv.jacobi(Rz, la, 1, la, W, S, 1e-14);
     sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
     sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
+    // the kept subspace is span(L) + span(U_act): a Ritz vector's rounding-level component
+    // along a locked direction u_j returns from M M^T amplified by sigma_j^2 (up to
+    // eps sigma_1 / sigma_i of the certificate's scale on steep cuts) yet lies inside the
+    // kept subspace -- measure the residual in the complement of span(L)
+    if (nlock > 0) project(PW, P);
     if (h.dry) {   // sizing pass: also reserve the G-form GEMMs' split-K slabs and the projection
       sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
       sv.gemm(G, "ij", {R, R}, Y, "ja", {R, l}, P, "ia", {R, l});

@@ -129,7 +129,11 @@ struct Cfg {
   static constexpr int WTN = BN / WN;
   static constexpr int MT = WTM / 8;            // 8x8 mma tiles per warp
   static constexpr int NT = WTN / 8;
-  static constexpr int PAD = 8;
+  // row pad 4 doubles: a half-warp's DMMA fragment load (rows kk+t, t = 0..3, 4 consecutive
+  // doubles each) then spans all 32 banks once (row stride 132 -> 8-bank offset per row);
+  // pad 8 (16-bank offset) made every fragment load 2-way conflicted (ncu: 9-20 M
+  // conflicts per chain launch) and the k-fast cp.async writes 8-way instead of 4-way
+  static constexpr int PAD = 4;
   static constexpr int LDA = BM + PAD;          // smem row (k) stride, doubles
   static constexpr int LDB = BN + PAD;
   static constexpr int STAGE_DOUBLES = BK * LDA + BK * LDB;
@@ -305,6 +309,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   double ss = 0.0;
   if (args.splits > 1) {
     double* __restrict__ P = args.part + ((size_t)blockIdx.z * M) * N;
+    const bool even = (N & 1) == 0;   // (m N + n) even: 16-byte aligned pair
 #pragma unroll
     for (int i = 0; i < C_::MT; ++i) {
       const int m = m0 + wm * C_::WTM + i * 8 + g;
@@ -312,8 +317,12 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
       for (int j = 0; j < C_::NT; ++j) {
         const int n = n0 + wn * C_::WTN + j * 8 + 2 * t;
         if (m < M) {
-          if (n < N) P[(size_t)m * N + n] = acc[i][j][0];
-          if (n + 1 < N) P[(size_t)m * N + n + 1] = acc[i][j][1];
+          if (even && n + 1 < N) {
+            *reinterpret_cast<double2*>(P + (size_t)m * N + n) = make_double2(acc[i][j][0], acc[i][j][1]);
+          } else {
+            if (n < N) P[(size_t)m * N + n] = acc[i][j][0];
+            if (n + 1 < N) P[(size_t)m * N + n + 1] = acc[i][j][1];
+          }
         }
       }
     }
@@ -328,6 +337,13 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
     for (int j = 0; j < C_::NT; ++j) {
       const int c = wn * C_::WTN + j * 8 + 2 * t;
       const int no0 = c_noff[c], no1 = c_noff[c + 1];
+      if (mo >= 0 && no0 >= 0 && no1 == no0 + 1 && ((mo + no0) & 1) == 0 && beta == 0.0) {
+        // the pair of accumulator columns is contiguous and 16-byte aligned in C: one vector store
+        const double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+        *reinterpret_cast<double2*>(Cg + mo + no0) = make_double2(v0, v1);
+        ss += v0 * v0 + v1 * v1;
+        continue;
+      }
       if (mo >= 0) {
         if (no0 >= 0) {
           double v = alpha * acc[i][j][0];
