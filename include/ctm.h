@@ -101,6 +101,12 @@ extern "C" {
 #define CTM_BOND_H 0         /* A left of B: 2x1 window                               */
 #define CTM_BOND_V 1         /* A above B: 1x2 window                                 */
 
+/* the four bonds of the 2-site unit cell (ctm_bond_update, ctm_trotter_step) */
+#define CTM_BOND_H1 0        /* A left of B (= CTM_BOND_H)                            */
+#define CTM_BOND_V1 1        /* A above B   (= CTM_BOND_V)                            */
+#define CTM_BOND_H2 2        /* B left of A                                           */
+#define CTM_BOND_V2 3        /* B above A                                             */
+
 /* directions (ctm_move) */
 #define CTM_LEFT 0
 #define CTM_RIGHT 1
@@ -286,6 +292,35 @@ int ctm_site_spins(ctm_handle h, const double* A, const double* B, const ctm_env
 
 int ctm_bond_energy(ctm_handle h, const double* A, const double* B, const ctm_env* env,
                     const double* hop, int bond, double* rho_out, double* e_out_host);
+
+/* ---------------------------------------------------------------------------------
+ * Imaginary-time evolution with the fast full update ("we used
+ * imaginary-time evolution method with a second-order Suzuki-Trotter decomposition ... we
+ * applied the fast full update scheme (FFU) ... to avoid recomputing the effective
+ * environments after each update step").  Readings R25-R30 fix what the paper
+ * leaves to its reference.
+ * --------------------------------------------------------------------------------- */
+/* ctm_trotter_gate: gate_out (d,d,d,d) device = exp(-delta h) of the bond operator hop
+ * (d,d,d,d) device as (s_i, s_j, s_i', s_j') (R25).  Asynchronous.  d^2 <= 16. */
+int ctm_trotter_gate(ctm_handle h, const double* hop, double delta, double* gate_out);
+
+/* ctm_bond_update: one FFU update of `bond` (CTM_BOND_H1/H2/V1/V2) of the sites A, B
+ * (d,D,D,D,D) device against the environment env (R26 reductions A = X aR, B = bL Y by SVD;
+ * R27 bond environment N of the 2x1 window, positivised; R28 gate, truncated-SVD start and
+ * `sweeps` ALS sweeps in the N metric, back to bond D).  A_out, B_out (device, same shapes,
+ * must not alias A, B) receive the Frobenius-normalised sites.  cost_host (nullable, 2
+ * doubles): the final N-weighted error ||aR bL - theta'||_N^2 and <theta'|N|theta'>.
+ * Synchronises the stream.  Needs a handle without CTM_FLAG_MOVE_ONLY. */
+int ctm_bond_update(ctm_handle h, const double* A, const double* B, const ctm_env* env, const double* gate,
+                    int bond, int sweeps, double* A_out, double* B_out, double* cost_host);
+
+/* ctm_trotter_step: one second-order Trotter step (R29) H1(delta/2) H2(delta/2) V1(delta/2)
+ * V2(delta) V1(delta/2) H2(delta/2) H1(delta/2) of the bond operator hop, A and B updated in
+ * place; refresh != 0: one CTM iteration (left, right, up, down) after every bond update
+ * (R30, the fast full update).  cost_host (nullable, 14 doubles): ctm_bond_update's pair per
+ * bond update.  Synchronises the stream. */
+int ctm_trotter_step(ctm_handle h, double* A, double* B, ctm_env* env, const double* hop, double delta, int sweeps,
+                     int refresh, double* cost_host);
 
 /* Algorithmic FP64 flops of one left move for square extents (SURVEY 8(a) closed form):
  * F_move = 2 (2 F_renv + 2 F_chain + 4 F_corner). */

@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libctm.so")
-SOURCES = ["ctm_abi.cu", "tc_gemm.cu", "svd.cu", "iso.cu", "kernels.cu"]
+SOURCES = ["ctm_abi.cu", "tc_gemm.cu", "svd.cu", "iso.cu", "kernels.cu", "ffu.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr"]

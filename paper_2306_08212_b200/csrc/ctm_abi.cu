@@ -18,54 +18,10 @@
 #include <exception>
 
 #include "ctm_internal.h"
+#include "ctm_tensor.h"
 
 namespace ctm {
 namespace {
-
-// ---------------------------------------------------------------------------------------
-// small tensor views
-// ---------------------------------------------------------------------------------------
-struct Ten {
-  double* p = nullptr;
-  std::vector<int> ext;
-  size_t size() const {
-    size_t n = 1;
-    for (int e : ext) n *= (size_t)e;
-    return n;
-  }
-};
-
-// ---------------------------------------------------------------------------------------
-// Environment access
-// ---------------------------------------------------------------------------------------
-Ten envC(const ctm_env* e, int x, int k) {
-  return Ten{e->C[x][k - 1], {e->ext[x][k - 1][0], e->ext[x][k - 1][1]}};
-}
-Ten envT(const ctm_env* e, int x, int k, int D) {
-  return Ten{e->T[x][k - 1], {e->ext[x][4 + k - 1][0], D, D, e->ext[x][4 + k - 1][1]}};
-}
-
-Operand op(const std::vector<const Ten*>& ts, const char* lab) {
-  Operand o;
-  o.lab = lab;
-  o.ext = ts[0]->ext;
-  for (auto* t : ts) o.p.push_back(t->p);
-  return o;
-}
-OutOperand out(const std::vector<Ten*>& ts, const char* lab, const std::vector<double*>& ss = {}) {
-  OutOperand o;
-  o.lab = lab;
-  o.ext = ts[0]->ext;
-  for (auto* t : ts) o.p.push_back(t->p);
-  o.sumsq = ss;
-  return o;
-}
-Ten alloc(Handle& h, std::vector<int> ext) {
-  Ten t;
-  t.ext = std::move(ext);
-  t.p = h.ws.take(t.size());
-  return t;
-}
 
 // Site tensor in the two orientations the chain needs (S2 / S5 operands).
 struct Site {
@@ -881,28 +837,6 @@ void left_move(Handle& h, const double* A, const double* B, ctm_env* env, const 
   h.ws.reset(mark);
 }
 
-// Quarter turns (clockwise storage: relabel k -> k+1, no data movement).
-void rotate_env_cw(ctm_env* e) {
-  ctm_env o = *e;
-  for (int x = 0; x < 2; ++x)
-    for (int k = 0; k < 4; ++k) {
-      int nk = (k + 1) % 4;
-      e->C[x][nk] = o.C[x][k];
-      e->T[x][nk] = o.T[x][k];
-      e->ext[x][nk][0] = o.ext[x][k][0];
-      e->ext[x][nk][1] = o.ext[x][k][1];
-      e->ext[x][4 + nk][0] = o.ext[x][4 + k][0];
-      e->ext[x][4 + nk][1] = o.ext[x][4 + k][1];
-    }
-}
-
-// Site leg permutation for n clockwise quarter turns: (s,u,l,d,r) -> turned.
-void rotate_site(Handle& h, const double* X, double* out, int turns) {
-  static const int perms[4][5] = {{0, 1, 2, 3, 4}, {0, 2, 3, 4, 1}, {0, 3, 4, 1, 2}, {0, 4, 1, 2, 3}};
-  const int* pm = perms[turns & 3];
-  permute(h, X, {h.prm.d, h.prm.D, h.prm.D, h.prm.D, h.prm.D}, {pm[0], pm[1], pm[2], pm[3], pm[4]}, out);
-}
-
 void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env, double* iso_out = nullptr) {
   static const int turns_for[4] = {0, 2, 3, 1};   // LEFT, RIGHT, UP, DOWN: cw turns bringing it left
   const int n = turns_for[dir];
@@ -926,6 +860,48 @@ void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env
     throw;
   }
   for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
+  h.ws.reset(mark);
+}
+
+// ---------------------------------------------------------------------------------------
+// Imaginary-time evolution (readings R25-R30): one FFU bond
+// update of any of the four bonds of the unit cell, by the same relabelling as the moves.
+//   H1: A left of B;  H2: B left of A (sublattice labels exchanged, reading R2);
+//   V1: A above B;    V2: B above A (picture turned counter-clockwise, sites turned back).
+// ---------------------------------------------------------------------------------------
+void swap_sublattices(ctm_env* e) {
+  std::swap(e->C[0], e->C[1]);
+  std::swap(e->T[0], e->T[1]);
+  std::swap(e->ext[0], e->ext[1]);
+}
+
+void ffu_update(Handle& h, const double* A, const double* B, const ctm_env* env, const double* gate, int bond,
+                int sweeps, double* A2, double* B2, double* cost) {
+  const size_t mark = h.ws.top;
+  ctm_env e = *env;
+  if (bond == CTM_BOND_H1) {
+    ffu_bond_update_h(h, A, B, &e, gate, sweeps, A2, B2, cost);
+  } else if (bond == CTM_BOND_H2) {
+    swap_sublattices(&e);
+    ffu_bond_update_h(h, B, A, &e, gate, sweeps, B2, A2, cost);
+  } else {
+    const size_t ns = (size_t)h.prm.d * h.prm.D * h.prm.D * h.prm.D * h.prm.D;
+    double* Ar = h.ws.take(ns);
+    double* Br = h.ws.take(ns);
+    double* a2 = h.ws.take(ns);
+    double* b2 = h.ws.take(ns);
+    rotate_site(h, A, Ar, 3);   // counter-clockwise quarter turn (= 3 clockwise)
+    rotate_site(h, B, Br, 3);
+    for (int i = 0; i < 3; ++i) rotate_env_cw(&e);
+    if (bond == CTM_BOND_V1) {
+      ffu_bond_update_h(h, Ar, Br, &e, gate, sweeps, a2, b2, cost);
+    } else {
+      swap_sublattices(&e);
+      ffu_bond_update_h(h, Br, Ar, &e, gate, sweeps, b2, a2, cost);
+    }
+    rotate_site(h, a2, A2, 1);   // back: one clockwise quarter turn
+    rotate_site(h, b2, B2, 1);
+  }
   h.ws.reset(mark);
 }
 
@@ -1264,6 +1240,12 @@ void size_workspace(Handle& h) {
         const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D;
         h.ws.take(2 * ns);
         ctm::bond_energy_impl(h, dummy, dummy, &env, dummy, nullptr);
+      });
+      optional([&]() {   // ctm_bond_update / ctm_trotter_step (gates + two site buffers)
+        const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D;
+        h.ws.take(4 * ns + 2 * (size_t)p.d * p.d * p.d * p.d);
+        double cost[2];
+        ctm::ffu_update(h, dummy, dummy, &env, dummy, CTM_BOND_V2, 1, dummy, dummy, cost);
       });
     }
   }
@@ -1623,6 +1605,56 @@ int ctm_converge(ctm_handle hh, const double* A, const double* B, ctm_env* env, 
       CTM_CUDA(cudaEventElapsedTime(&ms, h.ev[0], h.ev[1]));
       fill_stats(h, st, ms);
     }
+  });
+}
+
+int ctm_trotter_gate(ctm_handle hh, const double* hop, double delta, double* gate_out) {
+  return guarded(hh, [&](Handle& h) {
+    if (!hop || !gate_out) throw Error(CTM_E_ARG, "null pointer");
+    begin_call(h);
+    ctm::ffu_gate(h, hop, delta, gate_out);
+  });
+}
+
+int ctm_bond_update(ctm_handle hh, const double* A, const double* B, const ctm_env* env, const double* gate,
+                    int bond, int sweeps, double* A_out, double* B_out, double* cost_host) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || !gate || !A_out || !B_out || sweeps < 0 || bond < 0 || bond > 3)
+      throw Error(CTM_E_ARG, "bad argument");
+    if (A_out == A || A_out == B || B_out == A || B_out == B) throw Error(CTM_E_ARG, "outputs must not alias the sites");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    ctm::ffu_update(h, A, B, env, gate, bond, sweeps, A_out, B_out, cost_host);
+  });
+}
+
+int ctm_trotter_step(ctm_handle hh, double* A, double* B, ctm_env* env, const double* hop, double delta, int sweeps,
+                     int refresh, double* cost_host) {
+  return guarded(hh, [&](Handle& h) {
+    if (!A || !B || !env || !hop || sweeps < 0) throw Error(CTM_E_ARG, "bad argument");
+    begin_call(h);
+    ctm::check_env(env, h.prm);
+    const ctm_params& p = h.prm;
+    const size_t ns = (size_t)p.d * p.D * p.D * p.D * p.D, ng = (size_t)p.d * p.d * p.d * p.d;
+    double* g_half = h.ws.take(ng);
+    double* g_full = h.ws.take(ng);
+    double* A2 = h.ws.take(ns);
+    double* B2 = h.ws.take(ns);
+    ctm::ffu_gate(h, hop, 0.5 * delta, g_half);
+    ctm::ffu_gate(h, hop, delta, g_full);
+    // reading R29: H1(d/2) H2(d/2) V1(d/2) V2(d) V1(d/2) H2(d/2) H1(d/2); R30: one CTM
+    // iteration after every bond update (FFU)
+    static const int order[7] = {CTM_BOND_H1, CTM_BOND_H2, CTM_BOND_V1, CTM_BOND_V2, CTM_BOND_V1, CTM_BOND_H2,
+                                 CTM_BOND_H1};
+    for (int i = 0; i < 7; ++i) {
+      const double* g = i == 3 ? g_full : g_half;
+      ctm::ffu_update(h, A, B, env, g, order[i], sweeps, A2, B2, cost_host ? cost_host + 2 * i : nullptr);
+      CTM_CUDA(cudaMemcpyAsync(A, A2, ns * 8, cudaMemcpyDeviceToDevice, h.stream));
+      CTM_CUDA(cudaMemcpyAsync(B, B2, ns * 8, cudaMemcpyDeviceToDevice, h.stream));
+      if (refresh)
+        for (int dir : {CTM_LEFT, CTM_RIGHT, CTM_UP, CTM_DOWN}) ctm::move_dir(h, dir, A, B, env);
+    }
+    CTM_CUDA(cudaStreamSynchronize(h.stream));
   });
 }
 

@@ -144,6 +144,14 @@ void rho_finish(Handle& h, const double* rho, const double* hop, int d, double* 
 // (CTM_SVD_ISO: shifted CholQR3, no SVD).
 double svd_left(Handle& h, const double* mat, int R, int C, int n_keep, double* out, bool basis_only = false);
 
+// ffu.cu: the imaginary-time / fast-full-update bond update (readings
+// R25-R28): the horizontal bond A (left) - B (right) against the environment env; A2, B2
+// (device, d D^4 each) receive the Frobenius-normalised updated sites; cost (host, nullable)
+// = (final N-weighted error, <theta'|N|theta'>).  ffu_gate: g = exp(-delta h) (device d^4).
+void ffu_bond_update_h(Handle& h, const double* A, const double* B, const ctm_env* env, const double* gate,
+                       int sweeps, double* A2, double* B2, double* cost);
+void ffu_gate(Handle& h, const double* hop, double delta, double* g);
+
 // iso.cu: libctm's own truncated SVD (subspace iteration + CholQR + one-sided Jacobi).
 #define CTM_ISO_LMAX 160
 void iso_init_kernels();

@@ -25,6 +25,8 @@ CTM_FLAG_MOVE_ONLY = 2
 CTM_FLAG_PROFILE = 4
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
+CTM_BOND_H1, CTM_BOND_V1, CTM_BOND_H2, CTM_BOND_V2 = 0, 1, 2, 3
+BONDS = {"H1": CTM_BOND_H1, "V1": CTM_BOND_V1, "H2": CTM_BOND_H2, "V2": CTM_BOND_V2}
 CTM_TS_SVD, CTM_TS_BASIS = 0, 1
 DIRS = {"left": 0, "right": 1, "up": 2, "down": 3}
 CTM_E_ARG, CTM_E_CUDA, CTM_E_SOLVER, CTM_E_NONFINITE, CTM_E_NOMEM, CTM_E_UNSUPPORTED = 1, 2, 3, 4, 5, 6
@@ -95,6 +97,9 @@ def lib():
             "ctm_site_spins": (c_int, [P, P, P, POINTER(ctm_env), POINTER(c_double)]),
             "ctm_bond_energy": (c_int, [P, P, P, POINTER(ctm_env), P, c_int, P, POINTER(c_double)]),
             "ctm_move_flops": (c_double, [c_int, c_int, c_int, c_int, c_int]),
+            "ctm_trotter_gate": (c_int, [P, P, c_double, P]),
+            "ctm_bond_update": (c_int, [P, P, P, POINTER(ctm_env), P, c_int, c_int, P, P, POINTER(c_double)]),
+            "ctm_trotter_step": (c_int, [P, P, P, POINTER(ctm_env), P, c_double, c_int, c_int, POINTER(c_double)]),
             "ctm_kernel_count": (c_int64, [P]),
         }
         for name, (res, args) in sig.items():
@@ -108,7 +113,8 @@ def lib():
 def exported_symbols():
     return ["ctm_abi_version", "ctm_init", "ctm_set_workspace", "ctm_set_stream", "ctm_destroy",
             "ctm_last_error", "ctm_reduced_env", "ctm_ts_isometry", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
-            "ctm_iterate", "ctm_converge", "ctm_site_spins", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count"]
+            "ctm_iterate", "ctm_converge", "ctm_site_spins", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count",
+            "ctm_trotter_gate", "ctm_bond_update", "ctm_trotter_step"]
 
 
 def ctm_move_flops(d, D, chi, chi_p=None, chi_pp=None):
@@ -235,6 +241,29 @@ class CtmHandle:
         self._check(lib().ctm_bond_energy(self.h, _ptr(A), _ptr(B), byref(env.c), _ptr(h), bond, _ptr(rho_out),
                                           byref(e)))
         return e.value
+
+    # --- imaginary-time evolution -----------------------------------
+    def ctm_trotter_gate(self, hop, delta):
+        """exp(-delta h) on the device (d,d,d,d)."""
+        g = self.torch.empty_like(hop)
+        self._check(lib().ctm_trotter_gate(self.h, _ptr(hop), delta, _ptr(g)))
+        return g
+
+    def ctm_bond_update(self, A, B, env, gate, bond, sweeps, A_out=None, B_out=None):
+        """One FFU bond update (bond in 'H1','H2','V1','V2'); returns (A', B', (cost, tNt))."""
+        A_out = self.torch.empty_like(A) if A_out is None else A_out
+        B_out = self.torch.empty_like(B) if B_out is None else B_out
+        c = (c_double * 2)()
+        self._check(lib().ctm_bond_update(self.h, _ptr(A), _ptr(B), byref(env.c), _ptr(gate), BONDS[bond], sweeps,
+                                          _ptr(A_out), _ptr(B_out), c))
+        return A_out, B_out, (c[0], c[1])
+
+    def ctm_trotter_step(self, A, B, env, hop, delta, sweeps, refresh=True):
+        """One second-order Trotter step, A and B updated in place; returns 7 (cost, tNt)."""
+        c = (c_double * 14)()
+        self._check(lib().ctm_trotter_step(self.h, _ptr(A), _ptr(B), byref(env.c), _ptr(hop), delta, sweeps,
+                                           1 if refresh else 0, c))
+        return [(c[2 * i], c[2 * i + 1]) for i in range(7)]
 
     def iso_numel(self):
         p = self.params
