@@ -247,3 +247,31 @@ def test_reduced_env_with_injected_side_isometries(name):
     h.ctm_reduced_env(*args, M2, iso_in=side)
     torch.cuda.synchronize()
     assert rel_err(M2.cpu().numpy(), M1.cpu().numpy()) <= 1e-14
+
+
+def test_c4_dl_20_iterations_against_the_golden_oracle_trajectory():
+    """BASELINE config 4's 20-iteration energy check on the converging variant c4_dl (D = 8,
+    chi = 64, reading R16b): the GPU's gauge-invariant closures after every CTM iteration
+    against the oracle's trajectory stored in tests/golden/oracle_c4_dl.json (written by
+    tools/make_golden.py --dl from oracle/ only; the oracle's own perturbed-start spread on
+    this config stays ~1e-13, profiles/r02_spread_c4_dl.txt), at the north star's 1e-9."""
+    import json
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "oracle_c4_dl.json")))["c4_dl"]
+    cfg = ci.CONFIGS["c4_dl"]
+    g = ci.generate(cfg)
+    A, B = T_(g["A"]), T_(g["B"])
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    hop = T_(ci.heisenberg_h())
+    worst = 0.0
+    for it, ref in enumerate(gold["iterations"]):
+        h.ctm_iterate(A, B, env, 1)
+        got = {"norm_2x2": h.ctm_norm_2x2(A, B, env)[0],
+               "e_H": h.ctm_bond_energy(A, B, env, hop, ctm.CTM_BOND_H),
+               "e_V": h.ctm_bond_energy(A, B, env, hop, ctm.CTM_BOND_V)}
+        for k, v in ref.items():
+            err = abs(got[k] - v) / abs(v)
+            worst = max(worst, err)
+            assert err <= 1e-9, (it + 1, k, got[k], v)
+    print(f"c4_dl 20 iterations: worst relative deviation from the golden oracle trajectory {worst:.2e}")
