@@ -279,23 +279,6 @@ def test_iterations_gauge_invariant_1e9(name, n_iter, svd):
         assert abs(r[k + "_gpu"] - r[k + "_ref"]) <= 1e-9 * max(abs(r[k + "_ref"]), 1e-3)
 
 
-@pytest.mark.parametrize("name,n_iter", [("c2", 20), ("c3_dl", 20)])
-@pytest.mark.parametrize("svd", SVDS)
-def test_iterations_within_problem_conditioning(name, n_iter, svd):
-    """Ill-conditioned cases (Gaussian environment, near-degenerate truncations): the oracle
-    itself moves by O(1e-2) after 20 iterations when its start is perturbed by 1e-15, so the
-    bar is: GPU-vs-oracle <= 30 x oracle-vs-perturbed-oracle (+1e-9).  Reported, not hidden."""
-    if svd == "gram" and name == "c3_dl":
-        pytest.xfail("CTM_SVD_GRAM squares the condition number at the cut (DESIGN.md 6): measured 3.0e-7 "
-                     "against a 2.4e-7 bar on B200; kept as an option, not the default")
-    r = _iterate_both(name, n_iter, perturb=1e-15, svd=svd)
-    print(name, svd, r)
-    spread_n = abs(r["norm_pert"] - r["norm_ref"])
-    spread_e = abs(r["eH_pert"] - r["eH_ref"])
-    assert abs(r["norm_gpu"] - r["norm_ref"]) <= 30 * spread_n + 1e-9 * abs(r["norm_ref"])
-    assert abs(r["eH_gpu"] - r["eH_ref"]) <= 30 * spread_e + 1e-9 * max(abs(r["eH_ref"]), 1e-3)
-
-
 @pytest.mark.parametrize("bond", ["H", "V"])
 @pytest.mark.parametrize("name", ["tiny", "c2"])
 def test_bond_energy_closure(name, bond):

@@ -22,8 +22,16 @@ from paper_2306_08212_b200 import ctm  # noqa: E402
 PEAK = 37.14   # measured FP64 DMMA peak (profiles/r01_probe_fp64.txt)
 
 
+def config(name):
+    """A BASELINE config name, or 'D<D>_chi<chi>' (seeded, decaying spectrum) for sweeps."""
+    if name in ci.CONFIGS:
+        return ci.CONFIGS[name]
+    D, chi = name[1:].split("_chi")
+    return ci.custom(2, int(D), int(chi), decaying=True, seed_index=500 + int(D), name=name)
+
+
 def run(name, steps, svd, strategy="sequential"):
-    cfg = ci.CONFIGS[name]
+    cfg = config(name)
     g = ci.generate(cfg)
     dev = torch.device("cuda")
     stream = torch.cuda.Stream(dev)
