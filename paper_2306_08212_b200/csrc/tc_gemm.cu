@@ -13,21 +13,50 @@ namespace ctm {
 namespace {
 
 // Split-K reduction: C[off(m,n)] = alpha * sum_s P[b][s][m][n] (+ beta C), in split order.
+// Two consecutive n per thread (16-byte partial loads when N is even), the output offsets by
+// the magic-number divisions of the GEMM's own offset tables (no integer divide per element;
+// the plain-division version took 50 us for S6 at C4, four times its DRAM time).
 __global__ void splitk_reduce_kernel(const TcArgs args) {
   CTM_PDL_WAIT();
   const int b = blockIdx.y;
   const long long MN = (long long)args.M * args.N;
+  const int N = args.N;
+  const bool even = (N & 1) == 0;
+  const long long npair = even ? MN / 2 : MN;
   double ss = 0.0;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < MN; e += (long long)gridDim.x * blockDim.x) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < npair; q += (long long)gridDim.x * blockDim.x) {
+    const long long e = even ? 2 * q : q;
+    const int m = (int)(e / N), n = (int)(e - (long long)m * N);
+    int om, dummy, on;
+    tc::mode_offset2(m, args.nm, args.m_ext, args.m_mag, args.m_sh, args.c_m, args.c_m, om, dummy);
+    tc::mode_offset2(n, args.nn, args.n_ext, args.n_mag, args.n_sh, args.c_n, args.c_n, on, dummy);
     const double* P = args.part + (size_t)b * args.splits * MN + e;
-    double v = 0.0;
-    for (int s = 0; s < args.splits; ++s) v += P[(size_t)s * MN];
-    const int m = (int)(e / args.N), n = (int)(e - (long long)m * args.N);
-    const int off = tc::mode_offset(m, args.nm, args.m_ext, args.c_m) + tc::mode_offset(n, args.nn, args.n_ext, args.c_n);
-    v *= args.alpha;
-    if (args.beta != 0.0) v += args.beta * args.C[b][off];
-    args.C[b][off] = v;
-    ss += v * v;
+    if (even) {
+      double v0 = 0.0, v1 = 0.0;
+      for (int s = 0; s < args.splits; ++s) {
+        const double2 w = *reinterpret_cast<const double2*>(P + (size_t)s * MN);
+        v0 += w.x;
+        v1 += w.y;
+      }
+      int on1;
+      tc::mode_offset2(n + 1, args.nn, args.n_ext, args.n_mag, args.n_sh, args.c_n, args.c_n, on1, dummy);
+      v0 *= args.alpha;
+      v1 *= args.alpha;
+      if (args.beta != 0.0) {
+        v0 += args.beta * args.C[b][om + on];
+        v1 += args.beta * args.C[b][om + on1];
+      }
+      args.C[b][om + on] = v0;
+      args.C[b][om + on1] = v1;
+      ss += v0 * v0 + v1 * v1;
+    } else {
+      double v = 0.0;
+      for (int s = 0; s < args.splits; ++s) v += P[(size_t)s * MN];
+      v *= args.alpha;
+      if (args.beta != 0.0) v += args.beta * args.C[b][om + on];
+      args.C[b][om + on] = v;
+      ss += v * v;
+    }
   }
   if (args.sumsq[b] != nullptr) tc::block_sum_store(ss, args.sumsq[b] + blockIdx.x);
 }
@@ -127,7 +156,10 @@ struct CfgInfo {
   double eff;   // relative per-tile efficiency (bigger tiles reuse operands more)
 };
 // 0: 128x64 (8 warps 4x2), 1: 64x128 (8 warps 2x4), 2: 64x64 (4 warps 2x2); warp tile 32x32
+// (a 128x128 tile with 64x32 warp tiles -- 64 accumulator doubles, one CTA per SM -- measured
+// slower than 128x64 on every chain step but S3: profiles/r02_launches_inject_cfg3.txt)
 const CfgInfo kCfgs[] = {{128, 64, 2, 1.00}, {64, 128, 2, 1.00}, {64, 64, 3, 0.85}};
+constexpr int kNumCfgs = 3;
 constexpr int kSMs = 148;
 
 void launch_idx(Handle& h, int idx, const TcArgs& a, int gz) {
@@ -290,27 +322,32 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     const char* e = std::getenv("CTM_TC_CFG");
     return e ? std::atoi(e) : -1;
   }();
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < kNumCfgs; ++i) {
     if (forced >= 0 && i != forced) continue;
     const CfgInfo& c = kCfgs[i];
     long long tm = (M + c.BM - 1) / c.BM, tn = (N + c.BN - 1) / c.BN;
     long long tiles = tm * tn * batch;
     const long long slots = (long long)kSMs * c.per_sm;
-    int splits = 1;
+    // candidates: no split, and (when one wave is not filled) the split that fills two
+    // waves; a split pays its partial-tile traffic and the reduction (split_cost).  (S6 at
+    // C4 -- 256 tiles on 296 slots -- runs one full-K wave instead of 3 splits + reduction.)
+    int cand[2] = {1, 1};
     if (tiles < slots && K <= CTM_KTAB_MAX) {
       long long want = (2 * slots + tiles - 1) / tiles;
-      splits = (int)std::max(1LL, std::min({want, 8LL, ktiles_all / 4}));
+      cand[1] = (int)std::max(1LL, std::min({want, 8LL, ktiles_all / 4}));
     }
-    long long ctas = tiles * splits;
-    double fill = (double)M * N / ((double)tm * c.BM * tn * c.BN);
-    long long waves = (ctas + slots - 1) / slots;
-    double wave_eff = (double)ctas / (waves * (double)slots);
-    double split_cost = splits > 1 ? 0.97 : 1.0;
-    double score = fill * wave_eff * c.eff * split_cost;
-    if (score > best_score + 1e-9) {
-      best_score = score;
-      best = i;
-      best_splits = splits;
+    const double fill = (double)M * N / ((double)tm * c.BM * tn * c.BN);
+    for (int splits : cand) {
+      const long long ctas = tiles * splits;
+      const long long waves = (ctas + slots - 1) / slots;
+      const double wave_eff = (double)ctas / (waves * (double)slots);
+      const double split_cost = splits > 1 ? 0.97 : 1.0;
+      const double score = fill * wave_eff * c.eff * split_cost;
+      if (score > best_score + 1e-9) {
+        best_score = score;
+        best = i;
+        best_splits = splits;
+      }
     }
   }
   if (!C.sumsq.empty() && best_splits == 1) {
