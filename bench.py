@@ -125,12 +125,13 @@ def dist_setup(n_gpus):
 
 
 def traffic_bytes(cfg):
-    """DRAM bytes per contraction-only step of tc_gemm, measured by ncu --set full for C4
-    (profiles/r01_final_traffic.json); None for other configs or when the file is absent."""
-    path = os.path.join(ROOT, "profiles", "r01_final_traffic.json")
-    if cfg.name != "c4" or not os.path.exists(path):
-        return None
-    return json.load(open(path))["dram_bytes_per_step"]
+    """DRAM bytes per contraction-only step of tc_gemm, measured by ncu for C4 (the latest of
+    profiles/r02_traffic.json, profiles/r01_final_traffic.json); None for other configs."""
+    for name in ("r02_traffic.json", "r01_final_traffic.json"):
+        path = os.path.join(ROOT, "profiles", name)
+        if cfg.name == "c4" and os.path.exists(path):
+            return json.load(open(path))["dram_bytes_per_step"]
+    return None
 
 
 def max_over_ranks(vals, device=None):
