@@ -75,20 +75,39 @@ __global__ void scale_commit_kernel(Multi m, const double* __restrict__ ss, Part
   CTM_PDL_WAIT();
   const int y = blockIdx.y;
   __shared__ double inv_s;
-  if (threadIdx.x == 0) {
+  if (threadIdx.x < 32) {
+    // warp 0 sums the partials in a fixed order (lane-strided, then a fixed xor tree): deterministic,
+    // and 32x shorter than one thread's serial chain of global loads
     const double* p = ss + (size_t)y * CTM_SS_SLOTS;
     double acc = 0.0;
-    for (int j = 0; j < parts.n[y]; ++j) acc += p[j];
-    inv_s = 1.0 / sqrt(acc);
+    for (int j = threadIdx.x; j < parts.n[y]; j += 32) acc += p[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (threadIdx.x == 0) inv_s = 1.0 / sqrt(acc);
   }
   __syncthreads();
   const double inv = inv_s;
   const double* __restrict__ s = m.src[y];
   double* __restrict__ d = m.dst[y];
   const long long n = m.n[y];
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    d[i] = s[i] * inv;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if ((((uintptr_t)s | (uintptr_t)d) & 15) == 0) {
+    // 16-byte vector path for the even head, scalar tail
+    const long long n2 = n >> 1;
+    const double2* __restrict__ s2 = reinterpret_cast<const double2*>(s);
+    double2* __restrict__ d2 = reinterpret_cast<double2*>(d);
+    for (long long i = i0; i < n2; i += stride) {
+      double2 v = s2[i];
+      v.x *= inv;
+      v.y *= inv;
+      d2[i] = v;
+    }
+    i0 += 2 * n2;
+    if (i0 < n && i0 == 2 * n2) d[i0] = s[i0] * inv;
+    return;
+  }
+  for (long long i = i0; i < n; i += stride) d[i] = s[i] * inv;
 }
 
 __global__ void nonfinite_kernel(const double* __restrict__ p, long long n, int* cnt) {
