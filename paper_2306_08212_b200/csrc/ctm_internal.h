@@ -40,11 +40,6 @@ struct OutOperand {
   std::string lab;
   std::vector<int> ext;
   std::vector<double*> sumsq;   // optional fused sum of squares (one per batch entry)
-  // optional epilogue terms: C = alpha A B + beta C + gamma E, E (one per batch entry) laid out
-  // like C and never aliasing it; C may be read before it is written (an in-place recurrence)
-  double beta = 0.0;
-  double gamma = 0.0;
-  std::vector<const double*> E;
 };
 
 // Bump allocator over the caller-provided workspace.
@@ -189,27 +184,6 @@ void launch_k(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStrea
   const bool pdl = pdl_enabled();
   cfg.attrs = pdl ? at : nullptr;
   cfg.numAttrs = pdl ? 1 : 0;
-  CTM_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
-}
-
-// launch_k with a thread-block cluster of (1, 1, cluster_z) (tc_gemm's in-cluster split-K).
-template <typename... KArgs, typename... Args>
-void launch_kc(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, int cluster_z,
-               Args&&... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 1;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = (unsigned)cluster_z;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 2 : 1;
   CTM_CUDA(cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...));
 }
 

@@ -78,19 +78,10 @@ struct Solver {
   // C (m x n) = A * B with row-major operands given by label strings.
   void gemm(const double* A, const char* la, std::vector<int> ea, const double* B, const char* lb,
             std::vector<int> eb, double* C, const char* lc, std::vector<int> ec) {
-    gemm_epi(A, la, ea, B, lb, eb, C, lc, ec, 1.0, 0.0, 0.0, nullptr);
-  }
-  // C = alpha A B + beta C + gamma E (E laid out like C), the epilogue fused into tc_gemm
-  void gemm_epi(const double* A, const char* la, std::vector<int> ea, const double* B, const char* lb,
-                std::vector<int> eb, double* C, const char* lc, std::vector<int> ec, double alpha, double beta,
-                double gamma, const double* E) {
     Operand a{{A}, la, ea}, b{{B}, lb, eb};
     OutOperand c{{C}, lc, ec, {}};
-    c.beta = beta;
-    c.gamma = gamma;
-    if (gamma != 0.0) c.E = {E};
     const double f = h.flops;
-    contract(h, a, b, c, alpha);
+    contract(h, a, b, c);
     h.flops = f;   // solver work is not part of the move's algorithmic flops (R21)
   }
   // One CholQR pass on Y (m x n): S = Y^T Y, S (+shift) = R^T R, Y <- Y R^{-1}.
@@ -412,22 +403,22 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   // allowed only while that is <= 16 eps.  The Rayleigh-Ritz always uses M itself.
   double* G = h.ws.take((size_t)R * R);
   bool have_G = false;
-  // one Chebyshev degree with the three-term combine in the last GEMM's epilogue:
-  //   Yn = a (M M^T) Yc + b Yc + c Yo, written in place over Yo (Yo == nullptr: c = 0, Yn new)
-  auto cheb_step = [&](const double* Yc, double* Yn, bool old, double a, double b2, double c) {
-    if (have_G) {
-      sv.gemm_epi(G, "ij", {R, R}, Yc, "ja", {R, la}, Yn, "ia", {R, la}, a, old ? c : 0.0, b2, Yc);
-    } else {
-      sv.gemm(mat, "ic", {R, C}, Yc, "ia", {R, la}, Z, "ca", {C, la});
-      sv.gemm_epi(mat, "ic", {R, C}, Z, "ca", {C, la}, Yn, "ia", {R, la}, a, old ? c : 0.0, b2, Yc);
-    }
+  auto GYf = [&](const double* X, double* out) {
+    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, la}, out, "ia", {R, la});
+    else GY(X, out);
+  };
+  auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c) {
+    if (h.dry) return;
+    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, Pm, Yc, Yo, (long long)R * la, a, b2, c);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
   };
   // X <- X - L (L^T X): remove the locked directions from an active iterate (scratch: R x la)
   auto project = [&](double* X, double* scratch) {
     if (nlock == 0) return;
     sv.gemm(L, "ij", {R, nlock}, X, "ia", {R, la}, Tp, "ja", {nlock, la});
-    sv.gemm_epi(L, "ij", {R, nlock}, Tp, "ja", {nlock, la}, X, "ia", {R, la}, -1.0, 1.0, 0.0, nullptr);
-    (void)scratch;
+    sv.gemm(L, "ij", {R, nlock}, Tp, "ja", {nlock, la}, scratch, "ia", {R, la});
+    combine(X, scratch, X, nullptr, -1.0, 1.0, 0.0);
   };
   // columns [c0, c0 + nc) of a row-major R x ld matrix into a contiguous R x nc one
   auto copy_cols = [&](double* dst, int dld, int d0, const double* src, int sld, int c0, int nc) {
@@ -631,22 +622,23 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     const double s1c = 1.0 / xk;   // sigma_1 = e / (lambda_s - c)
     double sig = s1c;
     double *Yo = nullptr, *Yc = Y;
-    int done = 0;
+    double* bufs[2] = {Y1, Y2};
+    int nb = 0, done = 0;
     while (done < need) {
       const bool plain = plain_on && mb_plain > mb && need - done > tail;
       const int m = plain ? std::min(mb_plain, need - done - tail) : std::min(mb, need - done);
       for (int jj = 0; jj < m; ++jj) {
-        // the recurrence runs in place: Y_{j+1} overwrites Y_{j-1} (read by the same thread
-        // in the GEMM epilogue before the store), so two buffers carry it
-        double* Yn = Yo != nullptr ? Yo : (Yc == Y1 ? Y2 : Y1);
+        GYf(Yc, P);
+        double* Yn = bufs[nb];
+        nb ^= 1;
         if (Yo == nullptr) {
-          cheb_step(Yc, Yn, false, s1c / ce, -s1c, 0.0);
+          combine(Yn, P, Yc, nullptr, s1c / ce, -s1c, 0.0);
         } else {
           const double sn = 1.0 / (2.0 / s1c - sig);
-          cheb_step(Yc, Yn, true, 2.0 * sn / ce, -2.0 * sn, -sig * sn);
+          combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn);
           sig = sn;
         }
-        Yo = Yc;
+        Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
       }
       if (nlock > 0) {

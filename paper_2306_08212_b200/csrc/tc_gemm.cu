@@ -12,6 +12,57 @@
 namespace ctm {
 namespace {
 
+// Split-K reduction: C[off(m,n)] = alpha * sum_s P[b][s][m][n] (+ beta C), in split order.
+// Two consecutive n per thread (16-byte partial loads when N is even), the output offsets by
+// the magic-number divisions of the GEMM's own offset tables (no integer divide per element;
+// the plain-division version took 50 us for S6 at C4, four times its DRAM time).
+__global__ void splitk_reduce_kernel(const TcArgs args) {
+  CTM_PDL_WAIT();
+  const int b = blockIdx.y;
+  const long long MN = (long long)args.M * args.N;
+  const int N = args.N;
+  const bool even = (N & 1) == 0;
+  const long long npair = even ? MN / 2 : MN;
+  double ss = 0.0;
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < npair; q += (long long)gridDim.x * blockDim.x) {
+    const long long e = even ? 2 * q : q;
+    const int m = (int)(e / N), n = (int)(e - (long long)m * N);
+    int om, dummy, on;
+    tc::mode_offset2(m, args.nm, args.m_ext, args.m_mag, args.m_sh, args.c_m, args.c_m, om, dummy);
+    tc::mode_offset2(n, args.nn, args.n_ext, args.n_mag, args.n_sh, args.c_n, args.c_n, on, dummy);
+    const double* P = args.part + (size_t)b * args.splits * MN + e;
+    if (even) {
+      double v0 = 0.0, v1 = 0.0;
+      for (int s = 0; s < args.splits; ++s) {
+        const double2 w = *reinterpret_cast<const double2*>(P + (size_t)s * MN);
+        v0 += w.x;
+        v1 += w.y;
+      }
+      int on1;
+      tc::mode_offset2(n + 1, args.nn, args.n_ext, args.n_mag, args.n_sh, args.c_n, args.c_n, on1, dummy);
+      v0 *= args.alpha;
+      v1 *= args.alpha;
+      if (args.beta != 0.0) {
+        v0 += args.beta * args.C[b][om + on];
+        v1 += args.beta * args.C[b][om + on1];
+      }
+      args.C[b][om + on] = v0;
+      args.C[b][om + on1] = v1;
+      ss += v0 * v0 + v1 * v1;
+    } else {
+      double v = 0.0;
+      for (int s = 0; s < args.splits; ++s) v += P[(size_t)s * MN];
+      v *= args.alpha;
+      if (args.beta != 0.0) v += args.beta * args.C[b][om + on];
+      args.C[b][om + on] = v;
+      ss += v * v;
+    }
+  }
+  if (args.sumsq[b] != nullptr) tc::block_sum_store(ss, args.sumsq[b] + blockIdx.x);
+}
+
+
+
 struct Leg {
   char c;
   int ext;
@@ -67,8 +118,7 @@ void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
   auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>;   // attributes: tc_init_kernels
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
-  if (a.splits > 1) launch_kc(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a.splits, a);
-  else launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
+  launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
@@ -252,19 +302,17 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
   a.b_kfast = b_kfast;
   (void)c_nfast;
   a.alpha = alpha;
-  a.beta = C.beta;
-  a.gamma = C.gamma;
-  if (C.gamma != 0.0 && (int)C.E.size() != batch) throw Error(CTM_E_ARG, "contract: epilogue operand E missing");
+  a.beta = 0.0;
   for (int b = 0; b < batch; ++b) {
     a.A[b] = A.p[b];
     a.B[b] = B.p[b];
     a.C[b] = C.p[b];
-    a.E[b] = C.gamma != 0.0 ? C.E[b] : nullptr;
     a.sumsq[b] = C.sumsq.empty() ? nullptr : C.sumsq[b];
   }
   h.flops += 2.0 * (double)M * (double)N * (double)K * batch;
   a.splits = 1;
   a.ktiles_per_split = (int)((K + 15) / 16);
+  a.part = nullptr;
   // tile-config choice: maximise (wave efficiency) x (tile fill) x (per-tile efficiency),
   // then split K when one wave is not filled (deterministic split-K reduction).
   int best = 0, best_splits = 1;
@@ -302,17 +350,25 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
       }
     }
   }
-  if (!C.sumsq.empty()) {
-    // the fused sum of squares writes one partial per output tile (per split: one per
-    // cluster CTA) into a CTM_SS_SLOTS slot range: refuse a launch that would overflow into
-    // the neighbouring slots (fails in ctm_init's sizing pass)
-    const long long tiles =
-        ((M + kCfgs[best].BM - 1) / kCfgs[best].BM) * ((N + kCfgs[best].BN - 1) / kCfgs[best].BN) * best_splits;
+  if (!C.sumsq.empty() && best_splits == 1) {
+    // the fused sum of squares writes one partial per output tile into a CTM_SS_SLOTS slot
+    // range (the split-K path writes one per reduction CTA, <= 2 x 148): refuse a launch
+    // that would overflow into the neighbouring slots (fails in ctm_init's sizing pass)
+    const long long tiles = ((M + kCfgs[best].BM - 1) / kCfgs[best].BM) * ((N + kCfgs[best].BN - 1) / kCfgs[best].BN);
     if (tiles > CTM_SS_SLOTS)
       throw Error(CTM_E_ARG, "contract: " + std::to_string(tiles) + " output tiles exceed the " +
                                  std::to_string(CTM_SS_SLOTS) + " sum-of-squares slots (chi D too large)");
   }
-  if (h.dry) return 0;
+  if (h.dry) {
+    // sizing pass: reserve exactly the split-K slab the real launch will take (the tile /
+    // split choice above depends on shapes only); no slab when the launch is not split
+    if (best_splits > 1) {
+      const size_t mark = h.ws.top;
+      h.ws.take((size_t)batch * best_splits * M * N);
+      h.ws.reset(mark);
+    }
+    return 0;
+  }
   const bool prof = (h.prm.flags & CTM_FLAG_PROFILE) != 0;
   auto prof_begin = [&]() {
     if (!prof) return;
@@ -332,14 +388,20 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     h.prof_flops[h.prof_used] = flops;
     ++h.prof_used;
   };
-  if (best_splits > 1) {   // cluster split-K (tc_gemm.cuh): one launch, reduced in-cluster
+  if (best_splits > 1) {
+    const size_t mark = h.ws.top;
     a.splits = best_splits;
     a.ktiles_per_split = (int)((ktiles_all + best_splits - 1) / best_splits);
+    a.part = h.ws.take((size_t)batch * best_splits * M * N);
     prof_begin();
     launch_idx(h, best, a, batch * best_splits);
+    int rb = (int)std::min<long long>(2 * kSMs, ((long long)M * N + 255) / 256);
+    launch_k(splitk_reduce_kernel, dim3(rb, batch), dim3(256), 0, h.stream, a);
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
     prof_end(2.0 * (double)M * N * K * batch);
-    return (int)(((M + kCfgs[best].BM - 1) / kCfgs[best].BM) * ((N + kCfgs[best].BN - 1) / kCfgs[best].BN)) *
-           best_splits;
+    h.ws.reset(mark);
+    return rb;
   }
   // K beyond the shared-memory offset table: chunk the slowest k mode (beta = 1)
   const long long chunk = K > CTM_KTAB_MAX ? CTM_KTAB_MAX / k_inner : k_last;
@@ -352,8 +414,7 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     c.k_ext[lk] = (int)len;
     magic(c.k_ext[lk], c.k_mag[lk], c.k_sh[lk]);
     c.K = (int)(k_inner * len);
-    c.beta = j0 == 0 ? a.beta : 1.0;    // the caller's epilogue terms enter once, with the first chunk
-    c.gamma = j0 == 0 ? a.gamma : 0.0;
+    c.beta = j0 == 0 ? 0.0 : 1.0;
     c.splits = 1;
     c.ktiles_per_split = (c.K + 15) / 16;
     for (int b = 0; b < batch; ++b) {

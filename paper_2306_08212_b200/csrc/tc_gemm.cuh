@@ -1,6 +1,6 @@
 // tc_gemm.cuh -- FP64 tensor-contraction GEMM on the B200 DMMA pipe (sm_100a).
 //
-//   C[m, n] = alpha * sum_k A[m, k] * B[k, n]  (+ beta * C + gamma * E)
+//   C[m, n] = alpha * sum_k A[m, k] * B[k, n]  (+ beta * C)
 //
 // where m, n and k are multi-indices of up to CTM_MAXMODES modes each and every operand
 // is addressed through per-mode element strides, so the index permutations of the
@@ -23,16 +23,13 @@
 //  * epilogue: direct stores from the DMMA accumulator layout through per-row/column
 //    offset tables (any output permutation), fused sum of squares for the Frobenius
 //    normalisation (reading R13).
-//  * split-K (grid.z = batch x splits) for the small-M*N, large-K contractions (corners,
-//    the solver's R x l products): the splits of one output tile form a thread-block
-//    cluster (1, 1, splits <= 8); the partial tiles are reduced through distributed shared
-//    memory in split order inside the same launch (deterministic, no floating-point
-//    atomics, no workspace slab, no second kernel).
+//  * split-K (grid.z = batch x splits) for the small-M*N, large-K contractions (S3, S6,
+//    corners): partial tiles go to a workspace slab and a deterministic reduction kernel
+//    sums them in split order (no floating-point atomics on the data).
 //  * batch: one launch serves up to CTM_MAXBATCH problems with identical shapes/strides.
 #pragma once
 #include "pdl.cuh"
 #include <cstdint>
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #define CTM_MAXMODES 4
@@ -45,6 +42,7 @@ struct TcArgs {
   double* C[CTM_MAXBATCH];
   double* sumsq[CTM_MAXBATCH];   // nullable: per-CTA partial sums of squares of the final C values,
                                  // slot blockIdx.y*gridDim.x+blockIdx.x (deterministic reduction later)
+  double* part;                  // split-K partial slab [batch][split][M][N] (splits > 1)
   int M, N, K;
   int nm, nn, nk;
   int m_ext[CTM_MAXMODES], n_ext[CTM_MAXMODES], k_ext[CTM_MAXMODES];
@@ -58,9 +56,7 @@ struct TcArgs {
   int a_kfast, b_kfast;
   int splits, ktiles_per_split;
   double alpha;
-  double beta;     // C = alpha*A*B + beta*C + gamma*E (beta: K-chunked accumulation, or an in-place
-  double gamma;    // three-term recurrence; E: nullable, same layout as C, never aliases C)
-  const double* E[CTM_MAXBATCH];
+  double beta;     // C = alpha*A*B + beta*C (beta != 0 only for K-chunked accumulation)
 };
 
 namespace tc {
@@ -141,9 +137,6 @@ struct Cfg {
   static constexpr int LDA = BM + PAD;          // smem row (k) stride, doubles
   static constexpr int LDB = BN + PAD;
   static constexpr int STAGE_DOUBLES = BK * LDA + BK * LDB;
-  // split-K partial tile row stride (pad 8: a warp's 8 accumulator rows x 64 bytes store in
-  // four wavefronts)
-  static constexpr int LDR = BN + 8;
   static constexpr int PIPE_BYTES = STAGES * STAGE_DOUBLES * 8;
   static constexpr int TAB_BYTES = (2 * BM + 2 * BN) * 4 + 2 * CTM_KTAB_MAX * 4;
   static constexpr int SMEM_BYTES = PIPE_BYTES + TAB_BYTES;
@@ -312,88 +305,61 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   CTM_PDL_TRIGGER();
 
   // ---- epilogue: direct stores from the accumulator layout ---------------------------
-  const double alpha = args.alpha, beta = args.beta, gamma = args.gamma;
-  double* __restrict__ Cg = args.C[bz];
-  const double* __restrict__ Eg = args.E[bz];
+  const double alpha = args.alpha, beta = args.beta;
   double ss = 0.0;
-  // one accumulator pair (tile row r, tile columns c, c + 1): C = alpha acc + beta C + gamma E
-  auto store_pair = [&](int r, int c, double a0, double a1) {
-    const int mo = c_moff[r];
-    if (mo < 0) return;
-    const int no0 = c_noff[c], no1 = c_noff[c + 1];
-    double v0 = alpha * a0, v1 = alpha * a1;
-    if (no0 >= 0 && no1 == no0 + 1 && ((mo + no0) & 1) == 0) {
-      // the pair is contiguous and 16-byte aligned in C (and E): vector accesses
-      if (beta != 0.0) {
-        const double2 c2 = *reinterpret_cast<const double2*>(Cg + mo + no0);
-        v0 += beta * c2.x;
-        v1 += beta * c2.y;
-      }
-      if (gamma != 0.0) {
-        const double2 e2 = *reinterpret_cast<const double2*>(Eg + mo + no0);
-        v0 += gamma * e2.x;
-        v1 += gamma * e2.y;
-      }
-      *reinterpret_cast<double2*>(Cg + mo + no0) = make_double2(v0, v1);
-      ss += v0 * v0 + v1 * v1;
-      return;
-    }
-    if (no0 >= 0) {
-      if (beta != 0.0) v0 += beta * Cg[mo + no0];
-      if (gamma != 0.0) v0 += gamma * Eg[mo + no0];
-      Cg[mo + no0] = v0;
-      ss += v0 * v0;
-    }
-    if (no1 >= 0) {
-      if (beta != 0.0) v1 += beta * Cg[mo + no1];
-      if (gamma != 0.0) v1 += gamma * Eg[mo + no1];
-      Cg[mo + no1] = v1;
-      ss += v1 * v1;
-    }
-  };
   if (args.splits > 1) {
-    // split-K inside a thread-block cluster (1, 1, splits): the cluster's CTAs hold the same
-    // output tile over different K ranges.  Each parks its partial tile in its own (now free)
-    // pipeline buffers, and after a cluster barrier every CTA reduces 1/splits of the tile's
-    // rows by reading all partials through distributed shared memory in rank (= split) order
-    // -- the same summation order as a slab reduction, without the slab's HBM round trip or
-    // a second launch.
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    constexpr int LDR = C_::LDR;
-    static_assert(BM * LDR * 8 <= C_::PIPE_BYTES, "split-K tile exceeds the pipeline buffers");
-    __syncthreads();   // every warp is done with the pipeline buffers
+    double* __restrict__ P = args.part + ((size_t)blockIdx.z * M) * N;
+    const bool even = (N & 1) == 0;   // (m N + n) even: 16-byte aligned pair
 #pragma unroll
-    for (int i = 0; i < C_::MT; ++i)
+    for (int i = 0; i < C_::MT; ++i) {
+      const int m = m0 + wm * C_::WTM + i * 8 + g;
 #pragma unroll
-      for (int j = 0; j < C_::NT; ++j)
-        *reinterpret_cast<double2*>(pipe + (wm * C_::WTM + i * 8 + g) * LDR + wn * C_::WTN + j * 8 + 2 * t) =
-            make_double2(acc[i][j][0], acc[i][j][1]);
-    cluster.sync();
-    const int S = args.splits;
-    const int rpr = (BM + S - 1) / S, r0 = split * rpr, r1 = min(BM, r0 + rpr);
-    constexpr int HP = BN / 2;
-    for (int q = tid; q < (r1 - r0) * HP; q += THREADS) {
-      const int r = r0 + q / HP, c = 2 * (q % HP);
-      double v0 = 0.0, v1 = 0.0;
-      for (int s = 0; s < S; ++s) {
-        const double* peer = cluster.map_shared_rank(pipe, s);
-        const double2 w = *reinterpret_cast<const double2*>(peer + r * LDR + c);
-        v0 += w.x;
-        v1 += w.y;
+      for (int j = 0; j < C_::NT; ++j) {
+        const int n = n0 + wn * C_::WTN + j * 8 + 2 * t;
+        if (m < M) {
+          if (even && n + 1 < N) {
+            *reinterpret_cast<double2*>(P + (size_t)m * N + n) = make_double2(acc[i][j][0], acc[i][j][1]);
+          } else {
+            if (n < N) P[(size_t)m * N + n] = acc[i][j][0];
+            if (n + 1 < N) P[(size_t)m * N + n + 1] = acc[i][j][1];
+          }
+        }
       }
-      store_pair(r, c, v0, v1);
     }
-    if (args.sumsq[bz] != nullptr)
-      block_sum_store(ss, args.sumsq[bz] + (blockIdx.y * gridDim.x + blockIdx.x) * S + split);
-    cluster.sync();   // the peers are done reading this CTA's partial
     return;
   }
+  double* __restrict__ Cg = args.C[bz];
 #pragma unroll
-  for (int i = 0; i < C_::MT; ++i)
+  for (int i = 0; i < C_::MT; ++i) {
+    const int r = wm * C_::WTM + i * 8 + g;
+    const int mo = c_moff[r];
 #pragma unroll
-    for (int j = 0; j < C_::NT; ++j)
-      store_pair(wm * C_::WTM + i * 8 + g, wn * C_::WTN + j * 8 + 2 * t, acc[i][j][0], acc[i][j][1]);
+    for (int j = 0; j < C_::NT; ++j) {
+      const int c = wn * C_::WTN + j * 8 + 2 * t;
+      const int no0 = c_noff[c], no1 = c_noff[c + 1];
+      if (mo >= 0 && no0 >= 0 && no1 == no0 + 1 && ((mo + no0) & 1) == 0 && beta == 0.0) {
+        // the pair of accumulator columns is contiguous and 16-byte aligned in C: one vector store
+        const double v0 = alpha * acc[i][j][0], v1 = alpha * acc[i][j][1];
+        *reinterpret_cast<double2*>(Cg + mo + no0) = make_double2(v0, v1);
+        ss += v0 * v0 + v1 * v1;
+        continue;
+      }
+      if (mo >= 0) {
+        if (no0 >= 0) {
+          double v = alpha * acc[i][j][0];
+          if (beta != 0.0) v += beta * Cg[mo + no0];
+          Cg[mo + no0] = v;
+          ss += v * v;
+        }
+        if (no1 >= 0) {
+          double v = alpha * acc[i][j][1];
+          if (beta != 0.0) v += beta * Cg[mo + no1];
+          Cg[mo + no1] = v;
+          ss += v * v;
+        }
+      }
+    }
+  }
   if (args.sumsq[bz] != nullptr) block_sum_store(ss, args.sumsq[bz] + blockIdx.y * gridDim.x + blockIdx.x);
 }
 

@@ -14,7 +14,8 @@ import os
 from ctypes import POINTER, byref, c_double, c_int, c_int64, c_size_t, c_uint64, c_void_p
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libctm.so")
+# CTM_LIB_PATH: A/B experiments against another build of the same ABI (tools only)
+LIB_PATH = os.environ.get("CTM_LIB_PATH") or os.path.join(HERE, "libctm.so")
 
 CTM_OK = 0
 CTM_W_CLAMPED = 100
