@@ -113,14 +113,20 @@ ModeOut build_modes(std::vector<Leg> legs, int key, int op1, int op2) {
   return mo;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
-void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF, bool SEP>
+void launch_cfg3(Handle& h, const TcArgs& a, int gz) {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>;   // attributes: tc_init_kernels
+  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, SEP>;   // attributes: tc_init_kernels
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
   launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
+void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
+  if (a.ksep) launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, true>(h, a, gz);
+  else launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, false>(h, a, gz);
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
@@ -139,7 +145,9 @@ void launch_cfg(Handle& h, const TcArgs& a, int gz) {
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
 void set_attr_cfg2() {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF>,
+  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, false>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
+  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
 }
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
@@ -158,6 +166,9 @@ struct CfgInfo {
 // 0: 128x64 (8 warps 4x2), 1: 64x128 (8 warps 2x4), 2: 64x64 (4 warps 2x2); warp tile 32x32
 // (a 128x128 tile with 64x32 warp tiles -- 64 accumulator doubles, one CTA per SM -- measured
 // slower than 128x64 on every chain step but S3: profiles/r02_launches_inject_cfg3.txt)
+// (round 2: 64x128 / 128x64 with four 32x64 / 64x32 warp tiles -- cuBLAS's sm80 DGEMM tiles
+// for these shapes -- and 64x32 at three CTAs per SM were slower on every chain step but S3:
+// profiles/r02_launches_inject_tile_cfgs.txt)
 const CfgInfo kCfgs[] = {{128, 64, 2, 1.00}, {64, 128, 2, 1.00}, {64, 64, 3, 0.85}};
 constexpr int kNumCfgs = 3;
 constexpr int kSMs = 148;
@@ -300,6 +311,19 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
   for (int i = 0; i < a.nk; ++i) magic(a.k_ext[i], a.k_mag[i], a.k_sh[i]);
   a.a_kfast = a_kfast;
   a.b_kfast = b_kfast;
+  // separable k offsets: the 16-wide k-tiles (starting at multiples of 16) never straddle a
+  // k-mode boundary except by whole cycles of the inner modes -- some prefix product of the
+  // k extents divides 16 while the next one is a multiple of 16 (or K ends first)
+  a.ksep = [&] {
+    long long P = 1;
+    for (int e : mk.ext) {
+      if (16 % P != 0) return 0;
+      P *= e;
+      if (P % 16 == 0) return 1;
+    }
+    return 1;
+  }();
+  if (std::getenv("CTM_TC_NOSEP")) a.ksep = 0;   // A/B
   (void)c_nfast;
   a.alpha = alpha;
   a.beta = 0.0;
@@ -417,6 +441,7 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     c.beta = j0 == 0 ? 0.0 : 1.0;
     c.splits = 1;
     c.ktiles_per_split = (c.K + 15) / 16;
+    c.ksep = 0;   // (the chunk's last k extent differs from the planned one; closures only)
     for (int b = 0; b < batch; ++b) {
       c.A[b] = a.A[b] + j0 * sa_last;
       c.B[b] = a.B[b] + j0 * sb_last;

@@ -54,6 +54,7 @@ struct TcArgs {
   unsigned m_mag[CTM_MAXMODES], n_mag[CTM_MAXMODES], k_mag[CTM_MAXMODES];
   int m_sh[CTM_MAXMODES], n_sh[CTM_MAXMODES], k_sh[CTM_MAXMODES];
   int a_kfast, b_kfast;
+  int ksep;        // k offsets separable by 16-wide tiles (tc_gemm_kernel<..., SEP>)
   int splits, ktiles_per_split;
   double alpha;
   double beta;     // C = alpha*A*B + beta*C (beta != 0 only for K-chunked accumulation)
@@ -147,7 +148,7 @@ struct Cfg {
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "mma tiling");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool AKF, bool BKF>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool AKF, bool BKF, bool SEP>
 __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArgs args) {
   using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   constexpr int THREADS = C_::THREADS;
@@ -216,11 +217,28 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   for (int j = 0; j < C_::A_PER; ++j) a_row[j] = max(0, akf ? a_moff[a_var0 + j * a_step] : a_moff[a_fix]);
 #pragma unroll
   for (int j = 0; j < C_::B_PER; ++j) b_col[j] = max(0, bkf ? b_noff[b_var0 + j * b_step] : b_noff[b_fix]);
+  if constexpr (SEP) {
+    // separable k offsets (TcArgs::ksep): koff(k0 + kl) = koff(k0) + koff(kl) - koff(0) for every
+    // tile start k0, so each load's in-tile part is folded into its row / column offset here and
+    // a k-tile needs one table read per operand instead of one per load
+    const int a0 = a_row[0], b0 = b_col[0];
+#pragma unroll
+    for (int j = 0; j < C_::A_PER; ++j) {
+      const int kl = akf ? a_fix : (a_var0 + j * a_step);
+      a_row[j] = (akf ? a_row[j] : a0) + (kl < kcount ? a_koff[kl] - a_koff[0] : 0);
+    }
+#pragma unroll
+    for (int j = 0; j < C_::B_PER; ++j) {
+      const int kl = bkf ? b_fix : (b_var0 + j * b_step);
+      b_col[j] = (bkf ? b_col[j] : b0) + (kl < kcount ? b_koff[kl] - b_koff[0] : 0);
+    }
+  }
   const unsigned pipe_s = static_cast<unsigned>(__cvta_generic_to_shared(pipe));
 
   // one quarter of a stage's loads (part = 0..3), so they interleave with the DMMA steps
   constexpr int A_Q = (C_::A_PER + 3) / 4, B_Q = (C_::B_PER + 3) / 4;
-  auto load_part = [&](int stage, int kt, int part, bool full) {
+  // ta / tb (SEP): the tile's k offset in A / B, read once per k-tile by the caller
+  auto load_part = [&](int stage, int kt, int part, bool full, int ta, int tb) {
     const unsigned As = pipe_s + stage * C_::STAGE_DOUBLES * 8;
     const unsigned Bs = As + BK * C_::LDA * 8;
     const int k0 = kt * BK;   // relative to kbase
@@ -233,7 +251,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
         const int k = k0 + kl;
         const unsigned dst = As + (kl * C_::LDA + ml) * 8;
         if (full || k < kcount) {
-          cp_async8(dst, Ag + (a_row[akf ? j : 0] + a_koff[k]));
+          cp_async8(dst, Ag + (SEP ? a_row[j] + ta : a_row[akf ? j : 0] + a_koff[k]));
         } else {
           asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0));
         }
@@ -248,7 +266,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
         const int k = k0 + kl;
         const unsigned dst = Bs + (kl * C_::LDB + nl) * 8;
         if (full || k < kcount) {
-          cp_async8(dst, Bg + (b_col[bkf ? j : 0] + b_koff[k]));
+          cp_async8(dst, Bg + (SEP ? b_col[j] + tb : b_col[bkf ? j : 0] + b_koff[k]));
         } else {
           asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(dst), "d"(0.0));
         }
@@ -271,7 +289,8 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
   for (int s = 0; s < STAGES - 1; ++s) {
     if (s < ktiles) {
 #pragma unroll
-      for (int part = 0; part < 4; ++part) load_part(s, s, part, s < ktiles_full);
+      for (int part = 0; part < 4; ++part)
+        load_part(s, s, part, s < ktiles_full, SEP ? a_koff[s * BK] : 0, SEP ? b_koff[s * BK] : 0);
     }
     cp_async_commit();
   }
@@ -286,6 +305,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
     const bool nfull = nk < ktiles_full;
     const double* As = pipe + (kt % STAGES) * C_::STAGE_DOUBLES;
     const double* Bs = As + BK * C_::LDA;
+    const int ta = (SEP && do_load) ? a_koff[nk * BK] : 0, tb = (SEP && do_load) ? b_koff[nk * BK] : 0;
 #pragma unroll
     for (int kk = 0; kk < BK; kk += 4) {
       double af[C_::MT], bf[C_::NT];
@@ -293,7 +313,7 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
       for (int i = 0; i < C_::MT; ++i) af[i] = As[(kk + t) * C_::LDA + wm * C_::WTM + i * 8 + g];
 #pragma unroll
       for (int j = 0; j < C_::NT; ++j) bf[j] = Bs[(kk + t) * C_::LDB + wn * C_::WTN + j * 8 + g];
-      if (do_load) load_part(nk % STAGES, nk, kk / 4, nfull);
+      if (do_load) load_part(nk % STAGES, nk, kk / 4, nfull, ta, tb);
 #pragma unroll
       for (int i = 0; i < C_::MT; ++i)
 #pragma unroll
