@@ -113,49 +113,49 @@ ModeOut build_modes(std::vector<Leg> legs, int key, int op1, int op2) {
   return mo;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF, bool SEP>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB, bool AKF, bool BKF, bool SEP>
 void launch_cfg3(Handle& h, const TcArgs& a, int gz) {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, SEP>;   // attributes: tc_init_kernels
+  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, SEP, FB>;   // attributes: tc_init_kernels
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
   launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB, bool AKF, bool BKF>
 void launch_cfg2(Handle& h, const TcArgs& a, int gz) {
-  if (a.ksep) launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, true>(h, a, gz);
-  else launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, false>(h, a, gz);
+  if (a.ksep) launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, FB, AKF, BKF, true>(h, a, gz);
+  else launch_cfg3<BM, BN, BK, WM, WN, ST, MINB, FB, AKF, BKF, false>(h, a, gz);
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB>
 void launch_cfg(Handle& h, const TcArgs& a, int gz) {
   if (a.a_kfast) {
-    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, true>(h, a, gz);
-    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, false>(h, a, gz);
+    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, true>(h, a, gz);
+    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, false>(h, a, gz);
   } else {
-    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, true>(h, a, gz);
-    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, false>(h, a, gz);
+    if (a.b_kfast) launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, false, true>(h, a, gz);
+    else launch_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, false, false>(h, a, gz);
   }
 }
 
 // Dynamic shared memory above 48 KB is a per-device function attribute: set it for every
 // instantiation once per device (ctm_init, before any worker thread launches).
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool AKF, bool BKF>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB, bool AKF, bool BKF>
 void set_attr_cfg2() {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, false>,
+  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, false, FB>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
-  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, true>,
+  CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, true, FB>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
 }
-template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB>
 void set_attr_cfg() {
-  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, true>();
-  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, true, false>();
-  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, true>();
-  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, false, false>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, true>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, false>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, false, true>();
+  set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, false, false>();
 }
 
 struct CfgInfo {
@@ -166,18 +166,19 @@ struct CfgInfo {
 // 0: 128x64 (8 warps 4x2), 1: 64x128 (8 warps 2x4), 2: 64x64 (4 warps 2x2); warp tile 32x32
 // (a 128x128 tile with 64x32 warp tiles -- 64 accumulator doubles, one CTA per SM -- measured
 // slower than 128x64 on every chain step but S3: profiles/r02_launches_inject_cfg3.txt)
-// (round 2: 64x128 / 128x64 with four 32x64 / 64x32 warp tiles -- cuBLAS's sm80 DGEMM tiles
-// for these shapes -- and 64x32 at three CTAs per SM were slower on every chain step but S3:
-// profiles/r02_launches_inject_tile_cfgs.txt)
+// The two 8-warp configs double-buffer their DMMA fragments (FB: tc_gemm.cuh), the 4-warp one
+// does not (its 1024 x 160 solver GEMMs ran slower with it).  (round 2: 64x128 / 128x64 with
+// four 32x64 / 64x32 warp tiles -- cuBLAS's sm80 DGEMM tiles for these shapes -- and 64x32 at
+// three CTAs per SM were slower on every chain step: profiles/r02_launches_inject_tile_cfgs.txt)
 const CfgInfo kCfgs[] = {{128, 64, 2, 1.00}, {64, 128, 2, 1.00}, {64, 64, 3, 0.85}};
 constexpr int kNumCfgs = 3;
 constexpr int kSMs = 148;
 
 void launch_idx(Handle& h, int idx, const TcArgs& a, int gz) {
   switch (idx) {
-    case 0: launch_cfg<128, 64, 16, 4, 2, 3, 2>(h, a, gz); break;
-    case 1: launch_cfg<64, 128, 16, 2, 4, 3, 2>(h, a, gz); break;
-    default: launch_cfg<64, 64, 16, 2, 2, 3, 3>(h, a, gz); break;
+    case 0: launch_cfg<128, 64, 16, 4, 2, 3, 2, true>(h, a, gz); break;
+    case 1: launch_cfg<64, 128, 16, 2, 4, 3, 2, true>(h, a, gz); break;
+    default: launch_cfg<64, 64, 16, 2, 2, 3, 3, false>(h, a, gz); break;
   }
 }
 
@@ -190,9 +191,9 @@ void tc_init_kernels() {
   CTM_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
   if (done.count(dev)) return;
-  set_attr_cfg<128, 64, 16, 4, 2, 3, 2>();
-  set_attr_cfg<64, 128, 16, 2, 4, 3, 2>();
-  set_attr_cfg<64, 64, 16, 2, 2, 3, 3>();
+  set_attr_cfg<128, 64, 16, 4, 2, 3, 2, true>();
+  set_attr_cfg<64, 128, 16, 2, 4, 3, 2, true>();
+  set_attr_cfg<64, 64, 16, 2, 2, 3, 3, false>();
   done.insert(dev);
 }
 

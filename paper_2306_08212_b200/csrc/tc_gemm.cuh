@@ -148,7 +148,7 @@ struct Cfg {
   static_assert(WTM % 8 == 0 && WTN % 8 == 0 && BK % 4 == 0, "mma tiling");
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool AKF, bool BKF, bool SEP>
+template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB, bool AKF, bool BKF, bool SEP, bool FB>
 __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArgs args) {
   using C_ = Cfg<BM, BN, BK, WM, WN, STAGES, MINB>;
   constexpr int THREADS = C_::THREADS;
@@ -297,29 +297,70 @@ __global__ void __launch_bounds__(32 * WM * WN, MINB) tc_gemm_kernel(const TcArg
 
   // ---- main loop --------------------------------------------------------------------
   static_assert(BK == 16, "the load interleave assumes 4 DMMA k-steps per k-tile");
-  for (int kt = 0; kt < ktiles; ++kt) {
+  if constexpr (FB) {
+    // fragment double buffering (CUTLASS sm80 style): the fragments of k-step kk + 1 are read
+    // from shared memory while the DMMAs of kk issue; the stage barrier moves to the last k-step
+    // of the previous tile, right after its fragments are in registers, so the next tile's first
+    // fragments are prefetched under the last DMMAs of the current one
+    double af[2][C_::MT], bf[2][C_::NT];
+    auto frag = [&](int buf, int stage, int kk) {
+      const double* As = pipe + stage * C_::STAGE_DOUBLES;
+      const double* Bs = As + BK * C_::LDA;
+#pragma unroll
+      for (int i = 0; i < C_::MT; ++i) af[buf][i] = As[(kk + t) * C_::LDA + wm * C_::WTM + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < C_::NT; ++j) bf[buf][j] = Bs[(kk + t) * C_::LDB + wn * C_::WTN + j * 8 + g];
+    };
     cp_async_wait<STAGES - 2>();
     __syncthreads();
-    const int nk = kt + STAGES - 1;
-    const bool do_load = nk < ktiles;
-    const bool nfull = nk < ktiles_full;
-    const double* As = pipe + (kt % STAGES) * C_::STAGE_DOUBLES;
-    const double* Bs = As + BK * C_::LDA;
-    const int ta = (SEP && do_load) ? a_koff[nk * BK] : 0, tb = (SEP && do_load) ? b_koff[nk * BK] : 0;
+    if (ktiles > 0) frag(0, 0, 0);
+    for (int kt = 0; kt < ktiles; ++kt) {
+      const int nk = kt + STAGES - 1;
+      const bool do_load = nk < ktiles;
+      const bool nfull = nk < ktiles_full;
+      const int cur = kt % STAGES;
+      const int ta = (SEP && do_load) ? a_koff[nk * BK] : 0, tb = (SEP && do_load) ? b_koff[nk * BK] : 0;
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[C_::MT], bf[C_::NT];
+      for (int q = 0; q < 4; ++q) {
+        if (q < 3) frag((q + 1) & 1, cur, 4 * (q + 1));
+        if (do_load) load_part(nk % STAGES, nk, q, nfull, ta, tb);
+        if (q == 3) {
+          cp_async_commit();
+          cp_async_wait<STAGES - 2>();
+          __syncthreads();   // tile kt + 1 visible; every warp is done reading stage cur
+          if (kt + 1 < ktiles) frag(0, (kt + 1) % STAGES, 0);
+        }
 #pragma unroll
-      for (int i = 0; i < C_::MT; ++i) af[i] = As[(kk + t) * C_::LDA + wm * C_::WTM + i * 8 + g];
+        for (int i = 0; i < C_::MT; ++i)
 #pragma unroll
-      for (int j = 0; j < C_::NT; ++j) bf[j] = Bs[(kk + t) * C_::LDB + wn * C_::WTN + j * 8 + g];
-      if (do_load) load_part(nk % STAGES, nk, kk / 4, nfull, ta, tb);
-#pragma unroll
-      for (int i = 0; i < C_::MT; ++i)
-#pragma unroll
-        for (int j = 0; j < C_::NT; ++j) dmma(acc[i][j], af[i], bf[j]);
+          for (int j = 0; j < C_::NT; ++j) dmma(acc[i][j], af[q & 1][i], bf[q & 1][j]);
+      }
     }
-    cp_async_commit();
+  } else {
+    for (int kt = 0; kt < ktiles; ++kt) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      const int nk = kt + STAGES - 1;
+      const bool do_load = nk < ktiles;
+      const bool nfull = nk < ktiles_full;
+      const double* As = pipe + (kt % STAGES) * C_::STAGE_DOUBLES;
+      const double* Bs = As + BK * C_::LDA;
+      const int ta = (SEP && do_load) ? a_koff[nk * BK] : 0, tb = (SEP && do_load) ? b_koff[nk * BK] : 0;
+#pragma unroll
+      for (int kk = 0; kk < BK; kk += 4) {
+        double af[C_::MT], bf[C_::NT];
+#pragma unroll
+        for (int i = 0; i < C_::MT; ++i) af[i] = As[(kk + t) * C_::LDA + wm * C_::WTM + i * 8 + g];
+#pragma unroll
+        for (int j = 0; j < C_::NT; ++j) bf[j] = Bs[(kk + t) * C_::LDB + wn * C_::WTN + j * 8 + g];
+        if (do_load) load_part(nk % STAGES, nk, kk / 4, nfull, ta, tb);
+#pragma unroll
+        for (int i = 0; i < C_::MT; ++i)
+#pragma unroll
+          for (int j = 0; j < C_::NT; ++j) dmma(acc[i][j], af[i], bf[j]);
+      }
+      cp_async_commit();
+    }
   }
   cp_async_wait<0>();
   CTM_PDL_TRIGGER();
