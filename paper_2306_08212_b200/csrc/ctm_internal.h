@@ -113,8 +113,18 @@ struct Handle {
 // tc_gemm.cu: returns the number of sum-of-squares partials written per problem (slots
 // 0..n-1 of C.sumsq[b]; at most CTM_SS_SLOTS).
 constexpr int CTM_SS_SLOTS = 4096;
+// Deferred split-K reduction: when a contraction with a plain row-major [M][N] output runs
+// split-K, contract() may skip its reduction launch and hand the partial slab to the consumer
+// (p = slab [splits][M][N], summed in split order like splitk_reduce_kernel); p == nullptr: the
+// output was written to C as usual.  The slab stays valid in stream order until the next
+// launch that takes workspace.
+struct GemmPartials {
+  const double* p = nullptr;
+  int splits = 1;
+  long long mn = 0;
+};
 int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
-             double alpha = 1.0);
+             double alpha = 1.0, GemmPartials* defer = nullptr);
 // Per-device one-time kernel attributes (dynamic shared memory > 48 KB): called by ctm_init
 // on the handle's device before any worker thread exists (thread-safe, once per device).
 void tc_init_kernels();

@@ -58,6 +58,12 @@ void set_smem(const void* f, size_t bytes) {
   CTM_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
+// CTM_ISO_JAC_OLD=1: the previous Jacobi cluster shapes (A/B)
+static bool jac_old() {
+  static const bool on = std::getenv("CTM_ISO_JAC_OLD") != nullptr;
+  return on;
+}
+
 struct Solver {
   Handle& h;
   int* status;   // device: [0] CholQR pivot, [1] Jacobi failure, [2] Jacobi sweeps
@@ -77,11 +83,11 @@ struct Solver {
   }
   // C (m x n) = A * B with row-major operands given by label strings.
   void gemm(const double* A, const char* la, std::vector<int> ea, const double* B, const char* lb,
-            std::vector<int> eb, double* C, const char* lc, std::vector<int> ec) {
+            std::vector<int> eb, double* C, const char* lc, std::vector<int> ec, GemmPartials* defer = nullptr) {
     Operand a{{A}, la, ea}, b{{B}, lb, eb};
     OutOperand c{{C}, lc, ec, {}};
     const double f = h.flops;
-    contract(h, a, b, c);
+    contract(h, a, b, c, 1.0, defer);
     h.flops = f;   // solver work is not part of the move's algorithmic flops (R21)
   }
   // One CholQR pass on Y (m x n): S = Y^T Y, S (+shift) = R^T R, Y <- Y R^{-1}.
@@ -205,13 +211,28 @@ struct Solver {
     const int ms = max_sweeps < 0 ? 60 : max_sweeps;
     const double skip_tol = 1e-10;   // (1e-9 / 1e-8: no measurable change at C4 / C5)
     CTM_CUDA(cudaEventRecord(h.jev[0], h.stream));
-    if (n > LMAX) {   // C5: 8-CTA cluster, rows split eight ways
+    // cluster shapes from tools/bench_jacobi_cfg.cu (profiles/r02_jacobi_cluster_shapes.jsonl),
+    // us per sweep: l = 160: 2 CTAs x 8-lane groups 322 -> 4 x 4-lane 242; n = 128: one CTA 214
+    // -> 4 x 4-lane 150; l = 232: 8 x 4-lane 632 -> 8 x 2-lane 574
+    if (n > LMAX && jac_old()) {   // A/B (CTM_ISO_JAC_OLD): the previous shapes
       using J = JacCfg<8, 4, LMAX_BIG>;
       launch_k(jacobi_cluster_kernel<8, 4, LMAX_BIG>, dim3(8), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S,
                st, ms, tol, skip_tol);
-    } else if (n > 128) {   // register-resident 2-CTA cluster: 1.4x faster per sweep at l = 160
+    } else if (n > LMAX) {   // C5: 8-CTA cluster, rows split eight ways, 2-lane groups
+      using J = JacCfg<8, 2, LMAX_BIG>;
+      launch_k(jacobi_cluster_kernel<8, 2, LMAX_BIG>, dim3(8), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S,
+               st, ms, tol, skip_tol);
+    } else if (n > 128 && jac_old()) {
       using J = JacCfg<2, 8, LMAX>;
       launch_k(jacobi_cluster_kernel<2, 8, LMAX>, dim3(2), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S, st,
+               ms, tol, skip_tol);
+    } else if (n > 128) {   // register-resident 4-CTA cluster, 4-lane groups
+      using J = JacCfg<4, 4, LMAX>;
+      launch_k(jacobi_cluster_kernel<4, 4, LMAX>, dim3(4), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S, st,
+               ms, tol, skip_tol);
+    } else if (n > 32 && !jac_old() && !std::getenv("CTM_ISO_JAC_SMEM")) {   // 4-CTA cluster, 4-lane groups
+      using J = JacCfg<4, 4, 128>;
+      launch_k(jacobi_cluster_kernel<4, 4, 128>, dim3(4), dim3(J::THREADS), J::SMEM, h.stream, X, n, trans, ncols, U, S, st,
                ms, tol, skip_tol);
     } else if (n > 32 && !std::getenv("CTM_ISO_JAC_SMEM")) {   // register-resident, one CTA
       using J = JacCfg<1, 8, 128>;
@@ -227,7 +248,7 @@ struct Solver {
     jac_n = n;
     jac_max = ms;
     jac_slot = max_sweeps < 0 ? 2 : 5;   // status int index holding the sweep count
-    jac_ctas = n > LMAX ? 8 : (n > 128 ? 2 : 1);
+    jac_ctas = n > LMAX ? 8 : (jac_old() ? (n > 128 ? 2 : 1) : (n > 32 ? 4 : 1));
     h.count_kernel();
   }
   // Preconditioned one-sided Jacobi (Drmac & Veselic): the left singular vectors of
@@ -283,6 +304,9 @@ void iso_init_kernels() {   // per device, once (see tc_init_kernels)
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
   set_smem((const void*)jacobi_cluster_kernel<2, 8, LMAX>, JacCfg<2, 8, LMAX>::SMEM);
+  set_smem((const void*)jacobi_cluster_kernel<4, 4, LMAX>, JacCfg<4, 4, LMAX>::SMEM);
+  set_smem((const void*)jacobi_cluster_kernel<4, 4, 128>, JacCfg<4, 4, 128>::SMEM);
+  set_smem((const void*)jacobi_cluster_kernel<8, 2, LMAX_BIG>, JacCfg<8, 2, LMAX_BIG>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<1, 8, 128>, JacCfg<1, 8, 128>::SMEM);
   set_smem((const void*)jacobi_cluster_kernel<8, 4, LMAX_BIG>, JacCfg<8, 4, LMAX_BIG>::SMEM);
   done.insert(dev);
@@ -394,22 +418,30 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   float ms_rr = 0.f, ms_all = 0.f;
   int la = l, nlock = 0;                   // active columns, locked columns
   std::vector<double> s_lock;
-  auto GY = [&](const double* X, double* out) {   // out = M M^T X; leaves M^T X in Z (la columns)
+  // out = M M^T X; leaves M^T X in Z (la columns).  defer: the second GEMM may leave its split-K
+  // partials for the consumer (the Chebyshev combine sums them: one launch fewer per degree)
+  auto GY = [&](const double* X, double* out, GemmPartials* defer = nullptr) {
     sv.gemm(mat, "ic", {R, C}, X, "ia", {R, la}, Z, "ca", {C, la});
-    sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, la}, out, "ia", {R, la});
+    sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, la}, out, "ia", {R, la}, defer);
   };
   // Filter products through G = M M^T (one GEMM per degree instead of two) when the
   // kept spectrum is flat: the containment floor of the G-form is ~ eps (s_1/s_k)^2,
   // allowed only while that is <= 16 eps.  The Rayleigh-Ritz always uses M itself.
   double* G = h.ws.take((size_t)R * R);
   bool have_G = false;
+  GemmPartials fpart;   // the filter product's deferred split-K partials (GYf -> combine)
+  static const bool no_defer = std::getenv("CTM_ISO_NODEFER") != nullptr;   // A/B
   auto GYf = [&](const double* X, double* out) {
-    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, la}, out, "ia", {R, la});
-    else GY(X, out);
+    GemmPartials* d = no_defer ? nullptr : &fpart;
+    if (have_G) sv.gemm(G, "ij", {R, R}, X, "ja", {R, la}, out, "ia", {R, la}, d);
+    else GY(X, out, d);
   };
-  auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c) {
+  auto combine = [&](double* out, const double* Pm, const double* Yc, const double* Yo, double a, double b2, double c,
+                     const GemmPartials* part = nullptr) {
     if (h.dry) return;
-    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, Pm, Yc, Yo, (long long)R * la, a, b2, c);
+    const bool dp = part != nullptr && part->p != nullptr;
+    launch_k(cheb_combine_kernel, dim3(148), dim3(256), 0, h.stream, out, dp ? part->p : Pm, Yc, Yo, (long long)R * la, a,
+             b2, c, dp ? part->splits : 1);
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   };
@@ -632,10 +664,10 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
         double* Yn = bufs[nb];
         nb ^= 1;
         if (Yo == nullptr) {
-          combine(Yn, P, Yc, nullptr, s1c / ce, -s1c, 0.0);
+          combine(Yn, P, Yc, nullptr, s1c / ce, -s1c, 0.0, &fpart);
         } else {
           const double sn = 1.0 / (2.0 / s1c - sig);
-          combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn);
+          combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn, &fpart);
           sig = sn;
         }
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)

@@ -197,7 +197,8 @@ void tc_init_kernels() {
   done.insert(dev);
 }
 
-int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C, double alpha) {
+int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C, double alpha, GemmPartials* defer) {
+  if (defer) *defer = GemmPartials{};
   const int batch = (int)C.p.size();
   if (batch < 1 || batch > CTM_MAXBATCH || (int)A.p.size() != batch || (int)B.p.size() != batch)
     throw Error(CTM_E_ARG, "contract: bad batch");
@@ -420,6 +421,26 @@ int contract(Handle& h, const Operand& A, const Operand& B, const OutOperand& C,
     a.part = h.ws.take((size_t)batch * best_splits * M * N);
     prof_begin();
     launch_idx(h, best, a, batch * best_splits);
+    // deferred reduction: a single problem whose output is plain row-major [M][N] (the
+    // slab's own layout), alpha = 1, no fused sum of squares -- the consumer sums the partials
+    bool plain = defer != nullptr && batch == 1 && alpha == 1.0 && C.sumsq.empty();
+    long long s = 1;
+    for (int i = 0; plain && i < a.nn; ++i) {
+      plain = a.c_n[i] == s;
+      s *= a.n_ext[i];
+    }
+    for (int i = 0; plain && i < a.nm; ++i) {
+      plain = a.c_m[i] == s;
+      s *= a.m_ext[i];
+    }
+    if (plain) {
+      prof_end(2.0 * (double)M * N * K * batch);
+      defer->p = a.part;
+      defer->splits = best_splits;
+      defer->mn = (long long)M * N;
+      h.ws.reset(mark);
+      return 0;
+    }
     int rb = (int)std::min<long long>(2 * kSMs, ((long long)M * N + 255) / 256);
     launch_k(splitk_reduce_kernel, dim3(rb, batch), dim3(256), 0, h.stream, a);
     CTM_CUDA(cudaGetLastError());

@@ -94,13 +94,10 @@ int main(int argc, char** argv) {
     CK(cudaMemcpyFromSymbol(pr, chol_prof, sizeof(pr)));
     printf("{\"chol_phase_cycles\": {");
     long long prev = pr[0];
-    for (int b = 0; 32 * b < n; ++b)
-      for (int ph = 1; ph <= 3; ++ph) {
-        const long long t = pr[3 * b + ph];
-        if (32 * (b + 1) >= n && ph > 1) continue;
-        printf("\"b%d_%s\": %lld, ", b, ph == 1 ? "diag" : ph == 2 ? "panel" : "trail", t - prev);
-        prev = t;
-      }
+    for (int b = 0; 32 * b < n; ++b) {   // stamps 1 + 2b: panel + look-ahead done; 2 + 2b: diag || trailing done
+      printf("\"b%d_panel_la\": %lld, \"b%d_diag_trail\": %lld, ", b, pr[1 + 2 * b] - prev, b, pr[2 + 2 * b] - pr[1 + 2 * b]);
+      prev = pr[2 + 2 * b];
+    }
     printf("\"tail\": %lld, \"store\": %lld, \"pack\": %lld, \"dinv\": %lld}}\n", pr[40] - prev, pr[41] - pr[40], pr[43] - pr[41], pr[42] - pr[43]);
   }
 #endif
