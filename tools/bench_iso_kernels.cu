@@ -59,7 +59,7 @@ int main(int argc, char** argv) {
   CK(cudaMemcpy(dS, S.data(), 8ull * n * n, cudaMemcpyHostToDevice));
   CK(cudaMemcpy(dY, Y.data(), 8ull * m * n, cudaMemcpyHostToDevice));
   const size_t big = (size_t)LMAX * (LMAX + 1) * sizeof(double);
-  CK(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)big));
+  CK(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)chol_smem_bytes(LMAX)));
   CK(cudaFuncSetAttribute(jacobi_lsv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * LMAX * (LMAX + 1))));
   auto timeit = [&](auto f, int reps) {
     f();
