@@ -42,8 +42,18 @@ namespace {
 using namespace isok;
 // Block oversampling p (l = n + p): 32, or 48 when l exceeds the one-CTA limit LMAX anyway
 // (C5: 284 -> 269 ms per move; 16 / 24 were slower at C4, 48 / 64 at C4 cross the LMAX cliff).
+// solver tuning knobs for A/B experiments (environment, read once; defaults are the tuned values)
+static int knob_int(const char* name, int def) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : def;
+}
+static double knob_double(const char* name, double def) {
+  const char* e = std::getenv(name);
+  return e ? std::atof(e) : def;
+}
 static int iso_oversample(int n_keep) {
-  return (n_keep + 32 > LMAX && n_keep + 48 <= LMAX_BIG) ? 48 : 32;
+  static const int p = knob_int("CTM_ISO_P", 32);   // (A/B knob)
+  return (n_keep + p > LMAX && n_keep + 48 <= LMAX_BIG) ? 48 : p;
 }
 constexpr double EPS = 2.220446049250313e-16;
 
@@ -611,7 +621,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // whose cheap degrees (one GEMM each) buy back a check: flat C4 solves 14 -> 12.3 ms, the
     // move 56.6 -> 53.6 ms (3.0 over-filters; at l > LMAX -- C5 -- it measured 2-3% slower)
     // (1.6 / 2.5, or also for the second plan: within noise)
-    const double safety = (checks == 1 && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? 2.0 : 1.25;
+    static const double safe1 = knob_double("CTM_ISO_SAFE1", 2.0), safe = knob_double("CTM_ISO_SAFE", 1.25);
+    const double safety = (checks == 1 && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? safe1 : safe;
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
@@ -632,7 +643,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // by the replacement, the shifted tail and the residual certificate guard the result;
     // C5/chi=256 523 -> 400 ms, C5 232 -> 215 ms, no fallbacks; 1e12 within noise of 1e10;
     // a tail of 8 degrees: slower)
-    int mb_plain = std::max(1, std::min(12, (int)std::floor(std::log(1e10) / lg_deg)));
+    static const double spread_plain = knob_double("CTM_ISO_SPREAD_PLAIN", 1e10);
+    int mb_plain = std::max(1, std::min(12, (int)std::floor(std::log(spread_plain) / lg_deg)));
     // locked directions re-enter an active iterate through rounding (~eps) and the filter
     // amplifies them most (they sit above the active spectrum): project them out at every
     // orthonormalisation, often enough that they stay below 1e-6 of the active block
@@ -642,7 +654,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       mb = std::min(mb, mp);
       mb_plain = std::min(mb_plain, mp);
     }
-    const int tail = 6;
+    static const int tail = knob_int("CTM_ISO_TAIL", 6);
     // One Chebyshev recurrence over all `need` degrees; every mb degrees the current iterate
     // is re-orthonormalised (shifted CholQR, a basis is enough here) and the previous one is
     // multiplied by the same R^{-1}, so the three-term recurrence continues across the
