@@ -621,7 +621,10 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // whose cheap degrees (one GEMM each) buy back a check: flat C4 solves 14 -> 12.3 ms, the
     // move 56.6 -> 53.6 ms (3.0 over-filters; at l > LMAX -- C5 -- it measured 2-3% slower)
     // (1.6 / 2.5, or also for the second plan: within noise)
-    static const double safe1 = knob_double("CTM_ISO_SAFE1", 2.0), safe = knob_double("CTM_ISO_SAFE", 1.25);
+    // (round 2, session 2: re-tuned after the Jacobi / Cholesky speed-ups made a check cheaper than
+    //  over-filtering -- first plan 2.0 -> 1.4, later plans 1.25 -> 1.1, tail 6 -> 4: C4 move 37.4 -> 34.9 ms,
+    //  C5 182 -> ~173 ms, no fallbacks; profiles/r02_iso_knobs.jsonl)
+    static const double safe1 = knob_double("CTM_ISO_SAFE1", 1.4), safe = knob_double("CTM_ISO_SAFE", 1.1);
     const double safety = (checks == 1 && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? safe1 : safe;
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
@@ -654,7 +657,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       mb = std::min(mb, mp);
       mb_plain = std::min(mb_plain, mp);
     }
-    static const int tail = knob_int("CTM_ISO_TAIL", 6);
+    static const int tail = knob_int("CTM_ISO_TAIL", 4);
     // One Chebyshev recurrence over all `need` degrees; every mb degrees the current iterate
     // is re-orthonormalised (shifted CholQR, a basis is enough here) and the previous one is
     // multiplied by the same R^{-1}, so the three-term recurrence continues across the

@@ -7,10 +7,95 @@
 #include <mutex>
 #include <set>
 
+#include <cudaTypedefs.h>
+
 #include "ctm_internal.h"
+#include "tc_gemm_tma.cuh"
 
 namespace ctm {
 namespace {
+
+// ---- TMA staging (tc_gemm_tma.cuh) -------------------------------------------------------
+// CTM_TC_TMA=0 keeps every launch on the cp.async kernel (A/B).
+bool tma_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CTM_TC_TMA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 tma_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }();
+  return fn;
+}
+
+// One operand's tensor map [x_0, k_0 .. k_{nk-1}, x_1 .. x_{nx-1}] with box [tile + 4, k box, 1 ..]
+// (the 4 extra inner elements give the padded row pitch of tc_gemm's shared tiles); false when
+// the operand does not fit the TMA path.
+bool tma_map(CUtensorMap* map, const double* base, int nx, const int* xext, const int* xstr, int nk,
+             const int* kext, const int* kstr, int tile, int* rank_out) {
+  if (xstr[0] != 1 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+  if (nx > 1 && xext[0] % tile != 0) return false;   // a tile never straddles the contiguous mode
+  const int rank = 1 + nk + (nx - 1);
+  if (rank > 5) return false;
+  cuuint64_t dim[5], str[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  int d = 0;
+  dim[d] = (cuuint64_t)xext[0];
+  box[d++] = (cuuint32_t)(tile + 4);
+  // k box: whole prefix of the k modes covering the 16-wide k-tile (one mode of any extent: the
+  // tail arrives zero-filled)
+  int need = 16;
+  for (int j = 0; j < nk; ++j) {
+    dim[d] = (cuuint64_t)kext[j];
+    str[d - 1] = (cuuint64_t)kstr[j] * 8;
+    if (need > 1) {
+      if (nk > 1 && (kext[j] % need != 0 && need % kext[j] != 0)) return false;
+      const int b = std::min(need, kext[j]);
+      box[d] = (cuuint32_t)b;
+      need /= b;
+    } else {
+      box[d] = 1;
+    }
+    ++d;
+  }
+  if (nk > 1 && need != 1) return false;
+  for (int j = 1; j < nx; ++j) {
+    dim[d] = (cuuint64_t)xext[j];
+    str[d - 1] = (cuuint64_t)xstr[j] * 8;
+    box[d++] = 1;
+  }
+  for (int j = 0; j < rank - 1; ++j)
+    if (str[j] % 16 != 0 || str[j] >= (1ULL << 40)) return false;
+  auto enc = tma_encode();
+  if (enc == nullptr) return false;
+  if (enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dim, str, box, es,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  *rank_out = rank;
+  return true;
+}
+
+bool tma_plan(const TcArgs& a, int BM, int BN, int batch, TmaMaps& maps) {
+  if (!tma_enabled() || a.beta != 0.0 || a.a_kfast || a.b_kfast) return false;
+  for (int b = 0; b < batch; ++b) {
+    int ra = 0, rb = 0;
+    if (!tma_map(&maps.a[b], a.A[b], a.nm, a.m_ext, a.a_m, a.nk, a.k_ext, a.a_k, BM, &ra)) return false;
+    if (!tma_map(&maps.b[b], a.B[b], a.nn, a.n_ext, a.b_n, a.nk, a.k_ext, a.b_k, BN, &rb)) return false;
+    maps.a_rank = ra;
+    maps.b_rank = rb;
+  }
+  return true;
+}
 
 // Split-K reduction: C[off(m,n)] = alpha * sum_s P[b][s][m][n] (+ beta C), in split order.
 // Two consecutive n per thread (16-byte partial loads when N is even), the output offsets by
@@ -116,8 +201,20 @@ ModeOut build_modes(std::vector<Leg> legs, int key, int op1, int op2) {
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB, bool AKF, bool BKF, bool SEP>
 void launch_cfg3(Handle& h, const TcArgs& a, int gz) {
   using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
-  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, SEP, FB>;   // attributes: tc_init_kernels
   dim3 grid((a.N + BN - 1) / BN, (a.M + BM - 1) / BM, gz);
+  if constexpr (FB && !AKF && !BKF) {   // operand tiles by TMA where the operands allow it
+    // (only launches with at least a wave of output tiles: the solver's small GEMMs would pay
+    //  the host-side map encoding on their latency-bound critical path)
+    TmaMaps maps;
+    if ((long long)grid.x * grid.y * gz >= 256 && tma_plan(a, BM, BN, gz / a.splits, maps)) {
+      launch_k(tc::tc_gemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a,
+               maps);
+      CTM_CUDA(cudaGetLastError());
+      h.count_kernel();
+      return;
+    }
+  }
+  auto kern = tc::tc_gemm_kernel<BM, BN, BK, WM, WN, ST, MINB, AKF, BKF, SEP, FB>;   // attributes: tc_init_kernels
   launch_k(kern, grid, dim3(C_::THREADS), C_::SMEM_BYTES, h.stream, a);
   CTM_CUDA(cudaGetLastError());
   h.count_kernel();
@@ -152,6 +249,11 @@ void set_attr_cfg2() {
 }
 template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB, bool FB>
 void set_attr_cfg() {
+  if constexpr (FB) {
+    using C_ = tc::Cfg<BM, BN, BK, WM, WN, ST, MINB>;
+    CTM_CUDA(cudaFuncSetAttribute(tc::tc_gemm_tma_kernel<BM, BN, BK, WM, WN, ST, MINB>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES));
+  }
   set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, true>();
   set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, true, false>();
   set_attr_cfg2<BM, BN, BK, WM, WN, ST, MINB, FB, false, true>();
