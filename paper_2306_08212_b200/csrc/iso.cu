@@ -476,7 +476,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   }
   sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
   sv.cholqr(Y, R, l, 1, true, nullptr);
-  for (int it = 0; it < 4; ++it) {   // (2 or 6 steps: slower at C5 / C4)
+  static const int power_steps = knob_int("CTM_ISO_POWER", 4);
+  for (int it = 0; it < power_steps; ++it) {   // (2 or 6 steps: slower at C5 / C4)
     GY(Y, P);
     std::swap(Y, P);
     sv.cholqr(Y, R, l, 1, true, nullptr);
@@ -519,7 +520,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // the first Rayleigh-Ritz only seeds the filter bounds: a capped, loose Jacobi suffices
     // (one sweep: C4 74.5 -> 71 ms vs three; zero sweeps -- column norms only -- mis-set the
     // C5 filter bounds and cost a fallback)
-    if (checks == 1) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, 1);
+    static const int first_sweeps = knob_int("CTM_ISO_SWEEPS1", 1);
+    if (checks == 1) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, first_sweeps);
     else sv.jacobi(Rz, la, 1, la, W, S, 1e-14);
     sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
     sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
@@ -607,7 +609,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // smallest Ritz value of the active block), normalised at the k-th Ritz value; the error of
     // the slowest kept vector shrinks by x_k + sqrt(x_k^2 - 1) per degree.
     const double lk = s[kb - 1] * s[kb - 1], lb = s[la - 1] * s[la - 1], l1 = s[0] * s[0], lg = s1 * s1;
-    if (!have_G && lg <= 16.0 * lk) {   // (256 / 2500: within noise at C4/C5; not worth the floor)
+    static const double gform = knob_double("CTM_ISO_GFORM", 16.0);
+    if (!have_G && lg <= gform * lk) {   // (256 / 2500: within noise at C4/C5; not worth the floor)
       sv.gemm(mat, "ic", {R, C}, mat, "jc", {R, C}, G, "ij", {R, R});
       have_G = true;
     }
@@ -634,7 +637,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // so a larger per-block spread compounds from block to block until kept directions
     // drown (seen as Ritz residual blow-ups at l = 288).
     const double shift_rel = 11.0 * ((double)R * la + (double)la * (la + 1)) * EPS;
-    const double spread = std::min(1e6, 0.25 / std::sqrt(shift_rel));
+    static const double spread_cap = knob_double("CTM_ISO_SPREAD", 1e6);
+    const double spread = std::min(spread_cap, 0.25 / std::sqrt(shift_rel));
     const double lg_deg = std::acosh(std::max(x1, xk)) - std::acosh(xk) + 1e-12;   // log-spread per degree
     int mb = std::max(1, std::min(12, (int)std::floor(std::log(spread) / lg_deg)));
     // Longer blocks re-orthonormalised by one PLAIN CholQR pass (no shift: kappa(Q) ~ 1, so

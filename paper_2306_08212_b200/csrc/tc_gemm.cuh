@@ -16,7 +16,8 @@
 //    one CTA's prologue / epilogue / load bursts overlap the other's DMMA stream (the
 //    first version, one 128x128 CTA per SM, left the DMMA pipe idle ~47% of the time:
 //    profiles/r01_ncu_c4_chain_v1.txt).
-//  * operand staging: cp.async (LDGSTS, 8 B) gathers, 3-stage pipeline; each thread's
+//  * operand staging: TMA boxes for the launches whose operands admit them (tc_gemm_tma.cuh);
+//    otherwise cp.async (LDGSTS, 8 B) gathers, 3-stage pipeline; each thread's
 //    fixed row/column offsets live in registers, the k offsets in a shared-memory table;
 //    the thread mapping follows the operand's contiguous index (m/k-fast for A, k/n-fast
 //    for B) so every warp load is coalesced.
