@@ -1,0 +1,191 @@
+// fgemm.cuh -- the ISO solver's filter GEMM on the DMMA pipe (sm_100a), with the Chebyshev
+// three-term combine in its epilogue:
+//
+//   C (M x N) = alpha * op(A) X + beta * Y + gamma * W,    op(A) = A (M x K) or A^T (A: K x M)
+//
+// all operands dense row-major (leading dimensions lda, ldx, ldc, ldy; W shares ldc and may
+// alias C: each element is read before the same thread overwrites it).  The solver's
+// products are tall and skinny (M = K = chi D = 1024 at C4, N = the active block <= 160):
+// one 1024 x 160 output has only 48 tiles of tc_gemm's 64 x 64, so tc_gemm splits K eight
+// ways, writes 8 partial slabs and the combine kernel sums them -- two launches and ~10 MB
+// of partial traffic per Chebyshev degree.  Here a 32 x 32 tile keeps the full K per CTA
+// (160 CTAs at N = 160: one per SM), so the recurrence is one launch and no slab.
+//
+//  * 4 warps, 2 x 2 warp tiles of 16 x 16 (2 x 2 m8n8 DMMA tiles each), BK = 16, 4-stage
+//    cp.async pipeline (16-byte copies for A; 16-byte for X when its rows are 16-byte
+//    aligned, 8-byte otherwise), zero-fill (src-size 0) outside the matrix.
+//  * shared pitches = 4 (mod 16) doubles: the m8n8k4 fragment reads of a warp hit 16
+//    distinct 8-byte bank pairs per half-warp (conflict-free), for both A orientations.
+//  * fragment double buffering: k-step kk + 1's fragments are read under kk's DMMAs.
+#pragma once
+#include "pdl.cuh"
+#include <cuda_runtime.h>
+
+namespace fg {
+
+struct FgArgs {
+  const double* A;
+  const double* X;
+  double* C;
+  const double* Y;   // nullable (beta term)
+  const double* W;   // nullable (gamma term), may alias C
+  int lda, ldx, ldc, ldy;
+  int M, N, K;
+  double alpha, beta, gamma;
+};
+
+constexpr int BM = 32, BN = 32, BK = 16, STAGES = 4, THREADS = 128;
+constexpr int LDA_N = BK + 4;   // non-transposed A tile: As[m][k]
+constexpr int LDA_T = BM + 4;   // transposed A tile:     As[k][m]
+constexpr int LDB = BN + 4;     // X tile:                Bs[k][n]
+constexpr int A_DOUBLES = BM * LDA_N > BK * LDA_T ? BM * LDA_N : BK * LDA_T;
+constexpr int STAGE_DOUBLES = A_DOUBLES + BK * LDB;
+
+__device__ __forceinline__ void cp16(unsigned dst, const void* src, bool in) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(in ? 16 : 0));
+}
+__device__ __forceinline__ void cp8(unsigned dst, const void* src, bool in) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(in ? 8 : 0));
+}
+__device__ __forceinline__ void commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// TRANS: op(A) = A^T.  XVEC: X rows 16-byte aligned and N even (16-byte X copies).
+template <bool TRANS, bool XVEC>
+__global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
+  __shared__ __align__(16) double sm[STAGES * STAGE_DOUBLES];
+  const int tid = threadIdx.x;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int M = p.M, N = p.N, K = p.K;
+  const int ktiles = (K + BK - 1) / BK;
+  const unsigned sbase = (unsigned)__cvta_generic_to_shared(sm);
+  CTM_PDL_WAIT();
+
+  auto load = [&](int stage, int kt) {
+    const int k0 = kt * BK;
+    const unsigned As = sbase + stage * STAGE_DOUBLES * 8;
+    const unsigned Bs = As + A_DOUBLES * 8;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {   // A: 256 16-byte chunks
+      const int c = tid + THREADS * u;
+      if (!TRANS) {
+        const int r = c >> 3, kc = (c & 7) * 2;
+        const bool in = m0 + r < M && k0 + kc < K;
+        cp16(As + (r * LDA_N + kc) * 8, in ? p.A + (size_t)(m0 + r) * p.lda + k0 + kc : p.A, in);
+      } else {
+        const int kr = c >> 4, mc = (c & 15) * 2;
+        const bool in = k0 + kr < K && m0 + mc < M;
+        cp16(As + (kr * LDA_T + mc) * 8, in ? p.A + (size_t)(k0 + kr) * p.lda + m0 + mc : p.A, in);
+      }
+    }
+    if (XVEC) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {   // X: 256 16-byte chunks
+        const int c = tid + THREADS * u;
+        const int kr = c >> 4, nc = (c & 15) * 2;
+        const bool in = k0 + kr < K && n0 + nc < N;
+        cp16(Bs + (kr * LDB + nc) * 8, in ? p.X + (size_t)(k0 + kr) * p.ldx + n0 + nc : p.X, in);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {   // X: 512 8-byte elements
+        const int c = tid + THREADS * u;
+        const int kr = c >> 5, nc = c & 31;
+        const bool in = k0 + kr < K && n0 + nc < N;
+        cp8(Bs + (kr * LDB + nc) * 8, in ? p.X + (size_t)(k0 + kr) * p.ldx + n0 + nc : p.X, in);
+      }
+    }
+  };
+
+  const int warp = tid >> 5, lane = tid & 31;
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g = lane >> 2, t = lane & 3;
+  double acc[2][2][2] = {};
+  double af[2][2], bf[2][2];
+  auto frag = [&](int buf, int stage, int kk) {
+    const double* As = sm + stage * STAGE_DOUBLES;
+    const double* Bs = As + A_DOUBLES;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int m = wm * 16 + i * 8 + g;
+      af[buf][i] = TRANS ? As[(kk + t) * LDA_T + m] : As[m * LDA_N + kk + t];
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) bf[buf][j] = Bs[(kk + t) * LDB + wn * 16 + j * 8 + g];
+  };
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ktiles) load(s, s);
+    commit();
+  }
+  for (int kt = 0; kt < ktiles; ++kt) {
+    wait_group<STAGES - 2>();
+    __syncthreads();   // tile kt visible; every warp is done with the stage refilled below
+    const int nk = kt + STAGES - 1;
+    if (nk < ktiles) load(nk % STAGES, nk);
+    commit();
+    const int cur = kt % STAGES;
+    frag(0, cur, 0);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < 3) frag((q + 1) & 1, cur, 4 * (q + 1));
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[q & 1][i], bf[q & 1][j]);
+    }
+  }
+  wait_group<0>();
+  CTM_PDL_TRIGGER();
+
+  // epilogue: C = alpha acc + beta Y + gamma W (accumulator pair = columns 2t, 2t + 1)
+  const double alpha = p.alpha, beta = p.beta, gamma = p.gamma;
+  const bool vec = ((p.ldc | p.ldy) & 1) == 0;   // (host: ldy = ldc when Y is null)
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int m = m0 + wm * 16 + i * 8 + g;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int n = n0 + wn * 16 + j * 8 + 2 * t;
+      if (n >= N) continue;
+      double* c = p.C + (size_t)m * p.ldc + n;
+      const double* y = p.Y ? p.Y + (size_t)m * p.ldy + n : nullptr;
+      const double* w = p.W ? p.W + (size_t)m * p.ldc + n : nullptr;
+      if (vec && n + 1 < N) {
+        double2 v = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+        if (y) {
+          const double2 yy = *reinterpret_cast<const double2*>(y);
+          v.x = fma(beta, yy.x, v.x);
+          v.y = fma(beta, yy.y, v.y);
+        }
+        if (w) {
+          const double2 ww = *reinterpret_cast<const double2*>(w);
+          v.x = fma(gamma, ww.x, v.x);
+          v.y = fma(gamma, ww.y, v.y);
+        }
+        *reinterpret_cast<double2*>(c) = v;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          if (n + e >= N) break;
+          double v = alpha * acc[i][j][e];
+          if (y) v = fma(beta, y[e], v);
+          if (w) v = fma(gamma, w[e], v);
+          c[e] = v;
+        }
+      }
+    }
+  }
+}
+
+}  // namespace fg

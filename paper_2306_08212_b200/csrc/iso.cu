@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "ctm_internal.h"
+#include "fgemm.cuh"
 #include "iso_kernels.cuh"
 
 namespace ctm {
@@ -99,6 +100,32 @@ struct Solver {
     const double f = h.flops;
     contract(h, a, b, c, 1.0, defer);
     h.flops = f;   // solver work is not part of the move's algorithmic flops (R21)
+  }
+  // C (M x N, ld N) = alpha op(A) X + beta Y + gamma W on fgemm_kernel (fgemm.cuh): one
+  // launch, full K per CTA, no split-K slab.  A row-major with leading dimension lda,
+  // op(A) = A^T when trans; X (K x N), Y and W (M x N, nullable; W may alias C).  Returns
+  // false (nothing launched) when the operands miss its 16-byte A copies (the caller
+  // then takes the tc_gemm path).  CTM_ISO_FGEMM=0 disables it (A/B).
+  bool fgemm(const double* A, int lda, bool trans, int M, int K, const double* X, int N, double* C,
+             double alpha = 1.0, const double* Y = nullptr, double beta = 0.0, const double* W = nullptr,
+             double gamma = 0.0) {
+    static const bool on = knob_int("CTM_ISO_FGEMM", 1) != 0;
+    auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    if (!on || (lda & 1) || (trans ? (M & 1) : (K & 1)) || !al16(A)) return false;
+    if (h.dry || M == 0 || N == 0) return true;
+    fg::FgArgs a{A, X, C, Y, W, lda, N, N, N, M, N, K, alpha, beta, gamma};
+    const bool xvec = (N & 1) == 0 && al16(X);
+    const dim3 grid((N + fg::BN - 1) / fg::BN, (M + fg::BM - 1) / fg::BM);
+    if (trans) {
+      if (xvec) launch_k(fg::fgemm_kernel<true, true>, grid, dim3(fg::THREADS), 0, h.stream, a);
+      else launch_k(fg::fgemm_kernel<true, false>, grid, dim3(fg::THREADS), 0, h.stream, a);
+    } else {
+      if (xvec) launch_k(fg::fgemm_kernel<false, true>, grid, dim3(fg::THREADS), 0, h.stream, a);
+      else launch_k(fg::fgemm_kernel<false, false>, grid, dim3(fg::THREADS), 0, h.stream, a);
+    }
+    CTM_CUDA(cudaGetLastError());
+    h.count_kernel();
+    return true;
   }
   // One CholQR pass on Y (m x n): S = Y^T Y, S (+shift) = R^T R, Y <- Y R^{-1}.
   // replace: numerically dependent columns (pivot <= 1e-13 of the column's squared norm)
@@ -431,6 +458,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   // out = M M^T X; leaves M^T X in Z (la columns).  defer: the second GEMM may leave its split-K
   // partials for the consumer (the Chebyshev combine sums them: one launch fewer per degree)
   auto GY = [&](const double* X, double* out, GemmPartials* defer = nullptr) {
+    if (sv.fgemm(mat, C, true, C, R, X, la, Z) && sv.fgemm(mat, C, false, R, C, Z, la, out)) return;
     sv.gemm(mat, "ic", {R, C}, X, "ia", {R, la}, Z, "ca", {C, la});
     sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, la}, out, "ia", {R, la}, defer);
   };
@@ -679,15 +707,26 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       const bool plain = plain_on && mb_plain > mb && need - done > tail;
       const int m = plain ? std::min(mb_plain, need - done - tail) : std::min(mb, need - done);
       for (int jj = 0; jj < m; ++jj) {
-        GYf(Yc, P);
         double* Yn = bufs[nb];
         nb ^= 1;
+        double ca, cb, cc = 0.0;   // Yn = ca (M M^T) Yc + cb Yc + cc Yo
         if (Yo == nullptr) {
-          combine(Yn, P, Yc, nullptr, s1c / ce, -s1c, 0.0, &fpart);
+          ca = s1c / ce;
+          cb = -s1c;
         } else {
           const double sn = 1.0 / (2.0 / s1c - sig);
-          combine(Yn, P, Yc, Yo, 2.0 * sn / ce, -2.0 * sn, -sig * sn, &fpart);
+          ca = 2.0 * sn / ce;
+          cb = -2.0 * sn;
+          cc = -sig * sn;
           sig = sn;
+        }
+        // the recurrence in the filter GEMM's epilogue (one launch per degree on the G form)
+        const bool fused = have_G ? sv.fgemm(G, R, false, R, R, Yc, la, Yn, ca, Yc, cb, Yo, cc)
+                                  : (sv.fgemm(mat, C, true, C, R, Yc, la, Z) &&
+                                     sv.fgemm(mat, C, false, R, C, Z, la, Yn, ca, Yc, cb, Yo, cc));
+        if (!fused) {
+          GYf(Yc, P);
+          combine(Yn, P, Yc, Yo, ca, cb, cc, &fpart);
         }
         Yo = Yc;   // (the elementwise combine may overwrite its own Yold in place)
         Yc = Yn;
