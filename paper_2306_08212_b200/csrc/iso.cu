@@ -409,7 +409,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     }
     const double* U = W;
     if (tall) {
-      sv.gemm(Y, "ia", {R, n}, W, "ab", {n, n}, Ut, "ib", {R, n});
+      if (!sv.fgemm(Y, n, false, R, n, W, n, Ut)) sv.gemm(Y, "ia", {R, n}, W, "ab", {n, n}, Ut, "ib", {R, n});
       U = Ut;
     }
     signfix(h, U, n, 1, R, n_keep, out);
@@ -487,6 +487,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
   auto project = [&](double* X, double* scratch) {
     if (nlock == 0) return;
     sv.gemm(L, "ij", {R, nlock}, X, "ia", {R, la}, Tp, "ja", {nlock, la});
+    if (sv.fgemm(L, nlock, false, R, nlock, Tp, la, X, -1.0, X, 1.0)) return;   // X -= L Tp, one launch
     sv.gemm(L, "ij", {R, nlock}, Tp, "ja", {nlock, la}, scratch, "ia", {R, la});
     combine(X, scratch, X, nullptr, -1.0, 1.0, 0.0);
   };
@@ -502,7 +503,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
   }
-  sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
+  if (!sv.fgemm(mat, C, false, R, C, Z, l, Y)) sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
   sv.cholqr(Y, R, l, 1, true, nullptr);
   static const int power_steps = knob_int("CTM_ISO_POWER", 4);
   for (int it = 0; it < power_steps; ++it) {   // (2 or 6 steps: slower at C5 / C4)
@@ -551,8 +552,8 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     static const int first_sweeps = knob_int("CTM_ISO_SWEEPS1", 1);
     if (checks == 1) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, first_sweeps);
     else sv.jacobi(Rz, la, 1, la, W, S, 1e-14);
-    sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
-    sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
+    if (!sv.fgemm(Y, la, false, R, la, W, la, U)) sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
+    if (!sv.fgemm(P, la, false, R, la, W, la, PW)) sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
     // the kept subspace is span(L) + span(U_act): a Ritz vector's rounding-level component
     // along a locked direction u_j returns from M M^T amplified by sigma_j^2 (up to
     // eps sigma_1 / sigma_i of the certificate's scale on steep cuts) yet lies inside the
