@@ -39,7 +39,7 @@ B = torch.from_numpy(g["B"]).cuda()
 env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
 h.ctm_left_move(A, B, env, iso_in=iso)
 out = env.to_host()
-np.savez(sys.argv[3], **{k + "_" + key: v for k in ("C", "T") for key, v in out[k].items()})
+np.savez(sys.argv[3], **{f"{k}_{key[0]}{key[1]}": v for k in ("C", "T") for key, v in out[k].items()})
 """
 
 
