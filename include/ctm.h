@@ -46,7 +46,7 @@
 extern "C" {
 #endif
 
-#define CTM_ABI_VERSION 2
+#define CTM_ABI_VERSION 3
 
 /* status codes */
 #define CTM_OK 0
@@ -86,6 +86,18 @@ extern "C" {
 #define CTM_FLAG_CHECK_FINITE 1   /* scan every committed tensor for NaN/Inf         */
 #define CTM_FLAG_MOVE_ONLY 2      /* size the workspace for moves only (no closures)  */
 #define CTM_FLAG_PROFILE 4        /* time every contraction launch with CUDA events   */
+#define CTM_FLAG_WARM_START 8     /* CTM_SVD_ISO, sequential strategy: every truncating solve of a move
+                                     starts from the final block of the same solve site (direction,
+                                     absorption, cut) of the handle's previous move instead of a random
+                                     block.  A CTM iteration converges (N_CTM ~ 10-30 iterations),
+                                     so the previous subspace is a near-solution; the solve still ends
+                                     only on the residual certificate measured on the NEW matrix, so the
+                                     result is start-independent up to rounding.  The blocks (R x l
+                                     doubles per site, 48 sites) are device memory owned by the handle,
+                                     allocated at a site's first solve, freed by ctm_destroy; a site
+                                     whose shapes changed, and a warm solve that fails, start cold.
+                                     ctm_warm_reset forgets them.  Off by default (a move is then a
+                                     pure function of its inputs).                                  */
 
 /* reduced-env modes (ctm_reduced_env) */
 #define CTM_RENV_APPROX 0    /* {C'^1, T'^2, C'^2} with side isometries */
@@ -177,6 +189,12 @@ typedef struct {
   double ms_commit;
   double commit_bytes;
   int n_commit;
+  /* CTM_FLAG_WARM_START: truncating solves that started from their site's previous block, how
+     many of those were certified at their first Rayleigh-Ritz check (no filter degree at all),
+     and how many failed to converge and were redone from the cold start                      */
+  int n_warm;
+  int n_warm_hit;
+  int n_warm_retry;
 } ctm_move_stats;
 
 /* ctm_init: validate sizes, create the handle, report the workspace bytes needed by
@@ -328,6 +346,12 @@ double ctm_move_flops(int d, int D, int chi, int chi_p, int chi_pp);
 
 /* Number of libctm kernels launched since the handle was created (evidence counter). */
 int64_t ctm_kernel_count(ctm_handle h);
+
+/* CTM_FLAG_WARM_START: forget every solve site's stored block (the next move starts cold; the
+ * device buffers are kept for reuse).  Call it when A, B or the environment are replaced by
+ * unrelated ones -- not required for correctness (every solve is certified on its own matrix),
+ * only so that a stale block does not cost a failed warm solve.  CTM_OK also without the flag. */
+int ctm_warm_reset(ctm_handle h);
 
 #ifdef __cplusplus
 }

@@ -158,7 +158,8 @@ Iso ts_isometry(Handle& h, const Ten& Qt, int c1, int c2, Ten* Q2_keep, bool bas
   const int n1 = std::min(c1, P * K);
   Iso r;
   r.v1 = alloc(h, {P, K, n1});
-  r.gap1 = svd_left(h, Qt.p, P * K, Bd * F, n1, r.v1.p);
+  r.gap1 = svd_left(h, Qt.p, P * K, Bd * F, n1, r.v1.p);   // (warm-started from h.warm_slot, if set)
+  h.warm_slot = -1;                                         // stage one only
   Ten Q2 = alloc(h, {n1, Bd, F});
   contract(h, op({&r.v1}, "pka"), op({&Qt}, "pkbq"), out({&Q2}, "abq"));   // v^1 contracted into Q
   const int n2 = std::min(c2, n1 * Bd);
@@ -273,6 +274,8 @@ void sub_begin(Handle& s) {
   s.min_gap = std::numeric_limits<double>::infinity();
   s.n_svd = 0;
   s.n_svd_fallback = 0;
+  s.n_warm = s.n_warm_hit = s.n_warm_retry = 0;
+  s.warm_slot = -1;
   s.ms_jacobi = 0.0;
   s.jacobi_flops = 0.0;
   s.jacobi_cta_ms = 0.0;
@@ -286,6 +289,9 @@ void sub_merge(Handle& h, Handle& s) {
   h.min_gap = std::min(h.min_gap, s.min_gap);
   h.n_svd += s.n_svd;
   h.n_svd_fallback += s.n_svd_fallback;
+  h.n_warm += s.n_warm;
+  h.n_warm_hit += s.n_warm_hit;
+  h.n_warm_retry += s.n_warm_retry;
   h.ms_jacobi += s.ms_jacobi;
   h.jacobi_flops += s.jacobi_flops;
   h.jacobi_cta_ms += s.jacobi_cta_ms;
@@ -355,6 +361,8 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
     ri[x] = RenvIn{envC(env, x, 1), envT(env, x, 2, D), envC(env, x, 2), envT(env, x, 1, D), envT(env, x, 3, D), &st[x]};
   SideOut side[4];
   const bool reuse = cache != nullptr && cache->valid;
+  // CTM_FLAG_WARM_START: the solve sites of this (direction, absorption)
+  const int warm_base = (h.warm_dir * 2 + absorption) * CTM_WARM_SITES;
   // Two independent chains, one per cut type x: [left side TS on sub 2x || right side TS on
   // sub 2x+1] -> reduced env M_x + main TS on sub 2x.  Each chain waits only for its own
   // right-side task (host future + stream event), not for the other chain's side tasks.
@@ -363,6 +371,7 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
   auto right_task = [&](int x) {   // sub 2x+1: right side TS (+ its copy into the move's cache)
     try {
       Handle& sub = *h.subs[2 * x + 1];
+      if (h.warm) sub.warm_slot = warm_base + 3 * x + 1;
       side[2 * x + 1] = side_ts(sub, ri[x], false, p.chi_pp);
       if (cache != nullptr) {
         const SideOut& o = side[2 * x + 1];
@@ -384,6 +393,7 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
   };
   auto chain_task = [&](int x) {   // sub 2x: left side TS, then (after x's right side) a5
     Handle& s = *h.subs[2 * x];
+    if (h.warm) s.warm_slot = warm_base + 3 * x;
     side[2 * x] = side_ts(s, ri[x], true, p.chi_pp);
     if (reuse) side[2 * x + 1] = cache->side[x];
     else right_fut[x].get();   // host: the right-side task has enqueued everything
@@ -394,6 +404,7 @@ void isometry_stage(Handle& h, const ctm_env* env, const Site st[2], Iso V[2][2]
     }
     RenvOut ro = renv_finish(s, ri[x], side[2 * x], side[2 * x + 1]);
     static const bool main_svd2 = std::getenv("CTM_TS_MAIN_SVD") != nullptr;   // A/B: SVD stage two
+    if (h.warm) s.warm_slot = warm_base + 3 * x + 2;
     V[x][1 - x] = ts_isometry(s, ro.M, p.chi_p, p.chi, nullptr, !main_svd2);   // a5 (basis stage two: R24b)
   };
   std::vector<std::function<void()>> T;
@@ -853,12 +864,15 @@ void move_dir(Handle& h, int dir, const double* A, const double* B, ctm_env* env
     rotate_site(h, B, Br, n);
   }
   for (int i = 0; i < n; ++i) rotate_env_cw(env);
+  h.warm_dir = dir;   // the warm-start sites of this direction
   try {
     left_move(h, Ar, Br, env, nullptr, iso_out);
   } catch (...) {
+    h.warm_dir = 0;
     for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
     throw;
   }
+  h.warm_dir = 0;
   for (int i = 0; i < (4 - n) % 4; ++i) rotate_env_cw(env);
   h.ws.reset(mark);
 }
@@ -1118,6 +1132,8 @@ void begin_call(Handle& h) {
   h.min_gap = std::numeric_limits<double>::infinity();
   h.n_svd = 0;
   h.n_svd_fallback = 0;
+  h.n_warm = h.n_warm_hit = h.n_warm_retry = 0;
+  h.warm_slot = -1;
   h.ms_jacobi = 0.0;
   h.jacobi_flops = 0.0;
   h.jacobi_cta_ms = 0.0;
@@ -1148,6 +1164,9 @@ void fill_stats(Handle& h, ctm_move_stats* st, float ms_total) {
   st->min_gap = h.min_gap;
   st->n_svd = h.n_svd;
   st->n_svd_fallback = h.n_svd_fallback;
+  st->n_warm = h.n_warm;
+  st->n_warm_hit = h.n_warm_hit;
+  st->n_warm_retry = h.n_warm_retry;
   st->ms_jacobi = h.ms_jacobi;
   st->jacobi_flops = h.jacobi_flops;
   st->n_jacobi = h.n_jacobi;
@@ -1278,6 +1297,7 @@ void init_solver(Handle& h, const ctm_params* p) {
 void destroy_handle(Handle& h) {
   for (auto& s : h.subs) destroy_handle(*s);
   h.subs.clear();
+  h.warm.reset();   // frees the warm-start blocks (the workers' references went with subs)
   if (h.gesvdj_info) cusolverDnDestroyGesvdjInfo(h.gesvdj_info);
   if (h.solver_params) cusolverDnDestroyParams(h.solver_params);
   if (h.solver) cusolverDnDestroy(h.solver);
@@ -1326,6 +1346,11 @@ int ctm_init(ctm_handle* out, const ctm_params* p, uintptr_t stream, size_t* ws_
       s->owns_stream = true;
       init_solver(*s, &s->prm);
       h.subs.push_back(std::move(s));
+    }
+    if (h.prm.flags & CTM_FLAG_WARM_START) {
+      h.warm = std::make_shared<ctm::WarmStore>();
+      h.warm->slots.resize(4 * 2 * ctm::CTM_WARM_SITES);   // (direction, absorption, site); never resized
+      for (auto& s : h.subs) s->warm = h.warm;
     }
     size_workspace(h);
     if (ws_bytes) *ws_bytes = h.main_bytes + h.subs.size() * h.sub_bytes;
@@ -1378,6 +1403,16 @@ int ctm_destroy(ctm_handle hh) {
 const char* ctm_last_error(ctm_handle hh) { return hh ? hh->h.last_error.c_str() : "null handle"; }
 
 int64_t ctm_kernel_count(ctm_handle hh) { return hh ? hh->h.kernel_count : 0; }
+
+int ctm_warm_reset(ctm_handle hh) {
+  if (!hh) return CTM_E_ARG;
+  if (hh->h.warm)
+    for (auto& s : hh->h.warm->slots) {
+      s.valid = false;
+      s.miss = s.skip = 0;
+    }
+  return CTM_OK;
+}
 
 double ctm_move_flops(int d, int D, int chi, int chi_p, int chi_pp) {
   // Sum of 2 M N K over the contractions of one left move for square extents, exactly as

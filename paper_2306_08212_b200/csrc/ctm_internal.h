@@ -7,6 +7,7 @@
 
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -61,6 +62,32 @@ struct Arena {
   void reset(size_t to = 0) { top = to; }
 };
 
+// CTM_FLAG_WARM_START: the final iterated block (locked + active Ritz vectors, R x l) of every
+// truncating solve of a move, kept per solve site (direction, absorption, cut) and used as
+// the start block of the same site's next solve.  In a CTM iteration the environment -- and
+// with it every M -- converges, so the previous subspace is a near-solution; the solve still
+// ends only on the residual certificate of the NEW matrix (iso.cu), so the result does not
+// depend on the start beyond rounding.  Owned by the main handle, shared with its workers.
+struct WarmStore {
+  struct Slot {
+    double* p = nullptr;   // device, R x l row-major
+    size_t cap = 0;        // doubles allocated
+    int R = 0, l = 0;
+    bool valid = false;
+    // back-off: a site whose warm first check certified less than half of the wanted vectors (an
+    // environment that is not converging: the check was wasted) skips its next min(2^miss, 16)
+    // warm attempts (the block is still refreshed by every solve); a good attempt resets it
+    int miss = 0, skip = 0;
+  };
+  std::mutex mu;           // slot allocation (cudaMalloc from worker threads)
+  std::vector<Slot> slots;
+  ~WarmStore() {
+    for (auto& s : slots)
+      if (s.p) cudaFree(s.p);
+  }
+};
+constexpr int CTM_WARM_SITES = 6;   // per absorption: x = a, b times {left side, right side, main}
+
 struct Handle {
   ctm_params prm{};
   cudaStream_t stream = nullptr;
@@ -82,6 +109,13 @@ struct Handle {
   double min_gap = 1e300;
   int n_svd = 0;
   int n_svd_fallback = 0;               // CTM_SVD_ISO truncations handed to cuSOLVER
+  // CTM_FLAG_WARM_START (see WarmStore): the store (main handle owns, workers point to it), the
+  // slot of the next truncating solve on this handle (-1: cold start), the move direction
+  int n_warm = 0, n_warm_hit = 0;       // warm-started solves / of those certified at the first check
+  int n_warm_retry = 0;                 // warm-started solves that failed and were redone cold
+  std::shared_ptr<WarmStore> warm;
+  int warm_slot = -1;
+  int warm_dir = 0;
   double ms_jacobi = 0.0;               // ISO solver: Jacobi launches, event-timed
   double jacobi_flops = 0.0;
   double jacobi_cta_ms = 0.0;           // launch time x CTAs (1 CTA per SM): SM-weighted time

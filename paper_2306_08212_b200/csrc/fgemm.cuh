@@ -34,12 +34,23 @@ struct FgArgs {
   double alpha, beta, gamma;
 };
 
-constexpr int BM = 32, BN = 32, BK = 16, STAGES = 4, THREADS = 128;
+#ifndef FG_STAGES
+#define FG_STAGES 4
+#endif
+#ifndef FG_BK
+#define FG_BK 16
+#endif
+constexpr int BM = 32, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128;
+static_assert(BK == 16 || BK == 32, "fgemm: BK is 16 or 32");
+constexpr int KCH = BK / 2;                       // 16-byte chunks per k-row of a non-transposed A tile
+constexpr int A_ITERS = BM * BK / 2 / THREADS;    // 16-byte A chunks per thread and k-tile
+constexpr int X_ITERS = BK * BN / 2 / THREADS;    // 16-byte X chunks per thread and k-tile
 constexpr int LDA_N = BK + 4;   // non-transposed A tile: As[m][k]
 constexpr int LDA_T = BM + 4;   // transposed A tile:     As[k][m]
 constexpr int LDB = BN + 4;     // X tile:                Bs[k][n]
 constexpr int A_DOUBLES = BM * LDA_N > BK * LDA_T ? BM * LDA_N : BK * LDA_T;
 constexpr int STAGE_DOUBLES = A_DOUBLES + BK * LDB;
+constexpr size_t SMEM_BYTES = (size_t)STAGES * STAGE_DOUBLES * sizeof(double);
 
 __device__ __forceinline__ void cp16(unsigned dst, const void* src, bool in) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(in ? 16 : 0));
@@ -61,7 +72,7 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 // TRANS: op(A) = A^T.  XVEC: X rows 16-byte aligned and N even (16-byte X copies).
 template <bool TRANS, bool XVEC>
 __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
-  __shared__ __align__(16) double sm[STAGES * STAGE_DOUBLES];
+  extern __shared__ __align__(16) double sm[];   // SMEM_BYTES (dynamic: deeper pipelines pass 48 KB)
   const int tid = threadIdx.x;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int M = p.M, N = p.N, K = p.K;
@@ -74,10 +85,10 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     const unsigned As = sbase + stage * STAGE_DOUBLES * 8;
     const unsigned Bs = As + A_DOUBLES * 8;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {   // A: 256 16-byte chunks
+    for (int u = 0; u < A_ITERS; ++u) {   // A: BM BK / 2 16-byte chunks
       const int c = tid + THREADS * u;
       if (!TRANS) {
-        const int r = c >> 3, kc = (c & 7) * 2;
+        const int r = c / KCH, kc = (c % KCH) * 2;
         const bool in = m0 + r < M && k0 + kc < K;
         cp16(As + (r * LDA_N + kc) * 8, in ? p.A + (size_t)(m0 + r) * p.lda + k0 + kc : p.A, in);
       } else {
@@ -88,7 +99,7 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     }
     if (XVEC) {
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {   // X: 256 16-byte chunks
+      for (int u = 0; u < X_ITERS; ++u) {   // X: BK BN / 2 16-byte chunks
         const int c = tid + THREADS * u;
         const int kr = c >> 4, nc = (c & 15) * 2;
         const bool in = k0 + kr < K && n0 + nc < N;
@@ -96,7 +107,7 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
       }
     } else {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {   // X: 512 8-byte elements
+      for (int u = 0; u < 2 * X_ITERS; ++u) {   // X: BK BN 8-byte elements
         const int c = tid + THREADS * u;
         const int kr = c >> 5, nc = c & 31;
         const bool in = k0 + kr < K && n0 + nc < N;
@@ -136,8 +147,8 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     const int cur = kt % STAGES;
     frag(0, cur, 0);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      if (q < 3) frag((q + 1) & 1, cur, 4 * (q + 1));
+    for (int q = 0; q < BK / 4; ++q) {
+      if (q < BK / 4 - 1) frag((q + 1) & 1, cur, 4 * (q + 1));
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll

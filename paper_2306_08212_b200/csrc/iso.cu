@@ -117,11 +117,11 @@ struct Solver {
     const bool xvec = (N & 1) == 0 && al16(X);
     const dim3 grid((N + fg::BN - 1) / fg::BN, (M + fg::BM - 1) / fg::BM);
     if (trans) {
-      if (xvec) launch_k(fg::fgemm_kernel<true, true>, grid, dim3(fg::THREADS), 0, h.stream, a);
-      else launch_k(fg::fgemm_kernel<true, false>, grid, dim3(fg::THREADS), 0, h.stream, a);
+      if (xvec) launch_k(fg::fgemm_kernel<true, true>, grid, dim3(fg::THREADS), fg::SMEM_BYTES, h.stream, a);
+      else launch_k(fg::fgemm_kernel<true, false>, grid, dim3(fg::THREADS), fg::SMEM_BYTES, h.stream, a);
     } else {
-      if (xvec) launch_k(fg::fgemm_kernel<false, true>, grid, dim3(fg::THREADS), 0, h.stream, a);
-      else launch_k(fg::fgemm_kernel<false, false>, grid, dim3(fg::THREADS), 0, h.stream, a);
+      if (xvec) launch_k(fg::fgemm_kernel<false, true>, grid, dim3(fg::THREADS), fg::SMEM_BYTES, h.stream, a);
+      else launch_k(fg::fgemm_kernel<false, false>, grid, dim3(fg::THREADS), fg::SMEM_BYTES, h.stream, a);
     }
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
@@ -337,6 +337,10 @@ void iso_init_kernels() {   // per device, once (see tc_init_kernels)
   CTM_CUDA(cudaGetDevice(&dev));
   std::lock_guard<std::mutex> lock(mu);
   if (done.count(dev)) return;
+  set_smem((const void*)fg::fgemm_kernel<true, true>, fg::SMEM_BYTES);
+  set_smem((const void*)fg::fgemm_kernel<true, false>, fg::SMEM_BYTES);
+  set_smem((const void*)fg::fgemm_kernel<false, true>, fg::SMEM_BYTES);
+  set_smem((const void*)fg::fgemm_kernel<false, false>, fg::SMEM_BYTES);
   set_smem((const void*)chol_kernel, chol_smem_bytes(LMAX));
   set_smem((const void*)trsm_rows_kernel<(LMAX + 31) / 32>, rpk_size(LMAX) * sizeof(double));
   set_smem((const void*)jacobi_lsv_kernel, (size_t)LMAX * (LMAX + 1) * sizeof(double));
@@ -497,23 +501,45 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     CTM_CUDA(cudaMemcpy2DAsync(dst + d0, sizeof(double) * dld, src + c0, sizeof(double) * sld, sizeof(double) * nc, R,
                                cudaMemcpyDeviceToDevice, h.stream));
   };
-  // start: Y = orth(M Omega), then four plain steps Y <- orth(M M^T Y)
-  if (!h.dry) {
-    launch_k(fill_omega_kernel, dim3(148), dim3(256), 0, h.stream, Z, (long long)C * l, 0x5eed1234u);
-    CTM_CUDA(cudaGetLastError());
-    h.count_kernel();
+  // CTM_FLAG_WARM_START: this site's previous final block [locked | active Ritz vectors] as the
+  // start block (the whole l-dimensional space, oversampling columns included, so the first
+  // Rayleigh-Ritz also has good bounds for the filter).  It is orthonormal up to rounding, the
+  // first check is a full one (CholQR2, converged Jacobi, certificate on THIS matrix), and when
+  // every wanted vector passes the solve ends there; otherwise the filter is planned from the
+  // measured residuals like any later plan.
+  WarmStore::Slot* wslot = nullptr;
+  if (h.warm && h.warm_slot >= 0 && !h.dry) {
+    std::lock_guard<std::mutex> g(h.warm->mu);
+    if ((size_t)h.warm_slot < h.warm->slots.size()) wslot = &h.warm->slots[h.warm_slot];
   }
-  if (!sv.fgemm(mat, C, false, R, C, Z, l, Y)) sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
-  sv.cholqr(Y, R, l, 1, true, nullptr);
-  static const int power_steps = knob_int("CTM_ISO_POWER", 4);
-  for (int it = 0; it < power_steps; ++it) {   // (2 or 6 steps: slower at C5 / C4)
-    GY(Y, P);
-    std::swap(Y, P);
+  bool warm = wslot != nullptr && wslot->valid && wslot->R == R && wslot->l == l;
+  if (warm && wslot->skip > 0) {   // backing off after wasted first checks (see WarmStore::Slot)
+    --wslot->skip;
+    warm = false;
+  }
+  if (warm) {
+    CTM_CUDA(cudaMemcpyAsync(Y, wslot->p, sizeof(double) * R * l, cudaMemcpyDeviceToDevice, h.stream));
+    wslot->valid = false;   // re-validated by the store at the end of a successful solve
+    ++h.n_warm;
+  } else {
+    // start: Y = orth(M Omega), then four plain steps Y <- orth(M M^T Y)
+    if (!h.dry) {
+      launch_k(fill_omega_kernel, dim3(148), dim3(256), 0, h.stream, Z, (long long)C * l, 0x5eed1234u);
+      CTM_CUDA(cudaGetLastError());
+      h.count_kernel();
+    }
+    if (!sv.fgemm(mat, C, false, R, C, Z, l, Y)) sv.gemm(mat, "ic", {R, C}, Z, "ca", {C, l}, Y, "ia", {R, l});
     sv.cholqr(Y, R, l, 1, true, nullptr);
+    static const int power_steps = knob_int("CTM_ISO_POWER", 4);
+    for (int it = 0; it < power_steps; ++it) {   // (2 or 6 steps: slower at C5 / C4)
+      GY(Y, P);
+      std::swap(Y, P);
+      sv.cholqr(Y, R, l, 1, true, nullptr);
+    }
   }
   std::vector<double> s(l), r(k);
   double prev_worst = inf, prev_floor = inf;
-  int degrees = 4, checks = 0;
+  int degrees = warm ? 0 : 4, checks = 0;
   const int max_degrees = 400;
   const double cert = 8.0 * EPS * std::sqrt((double)C);
   bool plateau = false;
@@ -531,7 +557,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // Y and one shifted pass on Z suffice -- C4 57.0 -> 56.2 ms, C5 246 -> 240 ms; no pass on
     // Y at all mis-set the C5 bounds)
     // with locked vectors: project them out before each pass ("twice is enough")
-    const bool light = checks == 1;
+    const bool light = checks == 1 && !warm;
     if (light) {
       sv.cholqr(Y, R, la, 1, false, nullptr, true);
     } else if (nlock > 0 || h.dry) {
@@ -550,7 +576,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     // (one sweep: C4 74.5 -> 71 ms vs three; zero sweeps -- column norms only -- mis-set the
     // C5 filter bounds and cost a fallback)
     static const int first_sweeps = knob_int("CTM_ISO_SWEEPS1", 1);
-    if (checks == 1) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, first_sweeps);
+    if (light) sv.jacobi(Rz, la, 1, la, W, S, 1e-6, first_sweeps);
     else sv.jacobi(Rz, la, 1, la, W, S, 1e-14);
     if (!sv.fgemm(Y, la, false, R, la, W, la, U)) sv.gemm(Y, "ia", {R, la}, W, "ab", {la, la}, U, "ib", {R, la});
     if (!sv.fgemm(P, la, false, R, la, W, la, PW)) sv.gemm(P, "ia", {R, la}, W, "ab", {la, la}, PW, "ib", {R, la});
@@ -606,7 +632,18 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     if (debug)
       std::fprintf(stderr, "[iso]     certified %d of %d active wanted; unconverged: residual/s_i^2 %.3e  "
                            "residual/(s_1 s_i) %.3e (cert at %.3e)\n", j, ka, worst, worst_floor, cert);
-    if (!light && j == ka) break;
+    if (warm && checks == 1) {
+      if (2 * j >= ka) {
+        wslot->miss = 0;
+      } else {
+        wslot->miss = std::min(wslot->miss + 1, 4);
+        wslot->skip = 1 << wslot->miss;
+      }
+    }
+    if (!light && j == ka) {
+      if (warm && checks == 1) ++h.n_warm_hit;
+      break;
+    }
     // a plateau at the rounding floor (no further progress possible in FP64, within 64x of
     // the nominal floor constant) is accepted: the result is as accurate as the arithmetic
     if (checks > 2 && worst_floor <= 64.0 * cert && worst_floor > 0.5 * prev_floor) {
@@ -627,7 +664,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       nlock += j;
       la -= j;
       s.erase(s.begin(), s.begin() + j);
-    } else if (checks > 1) {
+    } else if (!light) {
       // filter the Ritz basis U (orthonormal): the filtered block stays nearly Ritz-ordered,
       // so the next Rayleigh-Ritz Jacobi starts close to diagonal and needs few sweeps
       // (after the capped first check W is not orthogonal: keep filtering Y itself)
@@ -657,7 +694,7 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     //  over-filtering -- first plan 2.0 -> 1.4, later plans 1.25 -> 1.1, tail 6 -> 4: C4 move 37.4 -> 34.9 ms,
     //  C5 182 -> ~173 ms, no fallbacks; profiles/r02_iso_knobs.jsonl)
     static const double safe1 = knob_double("CTM_ISO_SAFE1", 1.4), safe = knob_double("CTM_ISO_SAFE", 1.1);
-    const double safety = (checks == 1 && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? safe1 : safe;
+    const double safety = (light && l <= LMAX && (have_G || l1 <= 16.0 * lk)) ? safe1 : safe;
     int need = (int)std::ceil(safety * std::log(std::max(worst, 1e-300) / 1e-16) / std::log(rate)) + 2;
     need = std::max(2, std::min(need, max_degrees - degrees));
     // degree per orthonormalisation: keep the column scale spread (~T_m(x1)/T_m(xk)) <= 1e6
@@ -759,10 +796,25 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     signfix(h, Lt, k, 1, R, n_keep, out);
   }
   if (ka < la && s[ka] > 0.0) gap = (ka > 0 ? s[ka - 1] : s_lock.back()) / s[ka];
+  if (wslot != nullptr) {   // keep the final block [L | U] (nlock + la = l columns) for this site's next solve
+    if (wslot->cap < (size_t)R * l) {
+      std::lock_guard<std::mutex> g(h.warm->mu);
+      if (wslot->p) CTM_CUDA(cudaFree(wslot->p));
+      wslot->p = nullptr;
+      wslot->cap = 0;
+      CTM_CUDA(cudaMalloc(&wslot->p, sizeof(double) * R * l));
+      wslot->cap = (size_t)R * l;
+    }
+    copy_cols(wslot->p, l, 0, L, nlock, 0, nlock);
+    copy_cols(wslot->p, l, nlock, U, la, 0, la);
+    wslot->R = R;
+    wslot->l = l;
+    wslot->valid = true;
+  }
   if (debug)
     std::fprintf(stderr, "[iso] %d x %d keep %d: l=%d degrees=%d checks=%d locked=%d%s s1/sk=%.3g sl/sk=%.3g gap=%.5f ms=%.2f "
                          "rr_ms=%.2f last_sweeps=%d\n",
-                 R, C, n_keep, l, degrees, checks, nlock, plateau ? " (plateau)" : "",
+                 R, C, n_keep, l, degrees, checks, nlock, plateau ? " (plateau)" : warm ? " (warm)" : "",
                  (nlock ? s_lock[0] : s[0]) / (ka > 0 ? s[ka - 1] : s_lock.back()), s[la - 1] / (ka > 0 ? s[ka - 1] : s_lock.back()),
                  gap, ms_all, ms_rr, sv.last_sweeps);
   h.ws.reset(mark);
@@ -824,8 +876,21 @@ double iso_left_vectors(Handle& h, const double* mat, int R, int C, int n_keep, 
   *ok = true;
   const size_t mark = h.ws.top;
   const int n_svd = h.n_svd;
+  const int n_warm = h.n_warm;
   try {
-    return iso_left(h, mat, R, C, n_keep, out, signfix);
+    try {
+      return iso_left(h, mat, R, C, n_keep, out, signfix);
+    } catch (const IsoFail& e) {
+      if (h.n_warm == n_warm) throw;
+      // a warm-started solve that did not converge (its slot was invalidated at the start):
+      // redo it from the cold start before giving up on the solver
+      static const bool debug = std::getenv("CTM_ISO_DEBUG") != nullptr;
+      if (debug) std::fprintf(stderr, "[iso] %d x %d keep %d: warm start failed (%s), cold retry\n", R, C, n_keep, e.what());
+      h.ws.reset(mark);
+      h.n_svd = n_svd;
+      ++h.n_warm_retry;
+      return iso_left(h, mat, R, C, n_keep, out, signfix);
+    }
   } catch (const IsoFail& e) {
     static const bool debug = std::getenv("CTM_ISO_DEBUG") != nullptr;
     if (debug) std::fprintf(stderr, "[iso] %d x %d keep %d: fallback (%s)\n", R, C, n_keep, e.what());

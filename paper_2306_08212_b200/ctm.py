@@ -24,6 +24,7 @@ CTM_SVD_GESVDP, CTM_SVD_GESVDJ, CTM_SVD_GESVD, CTM_SVD_GRAM, CTM_SVD_ISO = 0, 1,
 CTM_FLAG_CHECK_FINITE = 1
 CTM_FLAG_MOVE_ONLY = 2
 CTM_FLAG_PROFILE = 4
+CTM_FLAG_WARM_START = 8
 CTM_RENV_APPROX, CTM_RENV_EXACT = 0, 1
 CTM_BOND_H, CTM_BOND_V = 0, 1
 CTM_BOND_H1, CTM_BOND_V1, CTM_BOND_H2, CTM_BOND_V2 = 0, 1, 2, 3
@@ -57,7 +58,8 @@ class ctm_move_stats(ctypes.Structure):
                 ("n_svd_fallback", c_int), ("ms_jacobi", c_double), ("jacobi_flops", c_double),
                 ("n_jacobi", c_int), ("jacobi_cta_ms", c_double),
                 ("cut_gap", (c_double * 2) * 2), ("side_gap", (c_double * 4) * 2),
-                ("ms_commit", c_double), ("commit_bytes", c_double), ("n_commit", c_int)]
+                ("ms_commit", c_double), ("commit_bytes", c_double), ("n_commit", c_int),
+                ("n_warm", c_int), ("n_warm_hit", c_int), ("n_warm_retry", c_int)]
 
     def as_dict(self):
         out = {}
@@ -102,6 +104,7 @@ def lib():
             "ctm_bond_update": (c_int, [P, P, P, POINTER(ctm_env), P, c_int, c_int, P, P, POINTER(c_double)]),
             "ctm_trotter_step": (c_int, [P, P, P, POINTER(ctm_env), P, c_double, c_int, c_int, POINTER(c_double)]),
             "ctm_kernel_count": (c_int64, [P]),
+            "ctm_warm_reset": (c_int, [P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -115,7 +118,7 @@ def exported_symbols():
     return ["ctm_abi_version", "ctm_init", "ctm_set_workspace", "ctm_set_stream", "ctm_destroy",
             "ctm_last_error", "ctm_reduced_env", "ctm_ts_isometry", "ctm_absorb_truncate", "ctm_left_move", "ctm_move",
             "ctm_iterate", "ctm_converge", "ctm_site_spins", "ctm_norm_2x2", "ctm_bond_energy", "ctm_move_flops", "ctm_kernel_count",
-            "ctm_trotter_gate", "ctm_bond_update", "ctm_trotter_step"]
+            "ctm_trotter_gate", "ctm_bond_update", "ctm_trotter_step", "ctm_warm_reset"]
 
 
 def ctm_move_flops(d, D, chi, chi_p=None, chi_pp=None):
@@ -174,6 +177,9 @@ class CtmHandle:
     @property
     def kernel_count(self):
         return lib().ctm_kernel_count(self.h)
+
+    def ctm_warm_reset(self):
+        self._check(lib().ctm_warm_reset(self.h))
 
     # --- ABI calls --------------------------------------------------------------------
     def ctm_absorb_truncate(self, T, X, Xbra, v1_in, v2_in, v1_out, v2_out, T_out):

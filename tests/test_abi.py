@@ -44,7 +44,7 @@ def test_binding_covers_header():
 
 def test_abi_version_and_flops(lib):
     from paper_2306_08212_b200 import ctm
-    assert ctm.lib().ctm_abi_version() == 2
+    assert ctm.lib().ctm_abi_version() == 3
     # F_move = 147.9 GF at d=2, D=8, chi=128
     f = ctm.ctm_move_flops(2, 8, 128)
     assert abs(f / 1e9 - 147.9) < 0.1

@@ -191,15 +191,20 @@ def shadow_move(env_h, A, B, direction, cfg, iso_flat, gpu_after, rng, log):
     log.append((direction, worst, ent, colerr))
 
 
-@pytest.mark.parametrize("name,n_iter", [("c2", 20), ("c3", 20), ("c4", 1)])
-def test_shadowed_trajectory(name, n_iter):
+@pytest.mark.parametrize("name,n_iter,warm", [("c2", 20, False), ("c3", 20, False), ("c4", 1, False),
+                                              ("c2", 20, True), ("c3", 6, True)])
+def test_shadowed_trajectory(name, n_iter, warm):
     """Every move of n_iter CTM iterations (left, right, up, down) shadowed by
     the oracle from the GPU's environment; closures on the GPU's environment after each
-    iteration (C4: after the iteration only)."""
+    iteration (C4: after the iteration only).  warm: the same bars with CTM_FLAG_WARM_START
+    (every truncating solve from the second iteration on starts from its site's previous
+    block; the oracle always solves from scratch)."""
     cfg = ci.CONFIGS[name]
     g = ci.generate(cfg)
     A, B = g["A"], g["B"]
-    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_CHECK_FINITE)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp,
+                      flags=ctm.CTM_FLAG_CHECK_FINITE | (ctm.CTM_FLAG_WARM_START if warm else 0))
+    n_warm = n_hit = n_retry = 0
     env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
     iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
     hop = ci.heisenberg_h()
@@ -213,6 +218,10 @@ def test_shadowed_trajectory(name, n_iter):
             # an uncertified ISO solve is redone by cuSOLVER gesvdp (counted, not hidden): parity
             # below holds either way; the count is reported
             fallbacks += st["n_svd_fallback"]
+            n_warm += st["n_warm"]
+            n_hit += st["n_warm_hit"]
+            n_retry += st["n_warm_retry"]
+            assert st["n_warm"] == (0 if not warm or it == 0 else st["n_warm"])
             shadow_move(before, A, B, direction, cfg, iso.cpu().numpy(), env.to_host(), rng, log)
         e_h = env.to_host()
         for bond, bname in ((ctm.CTM_BOND_H, "H"), (ctm.CTM_BOND_V, "V")):
@@ -226,7 +235,11 @@ def test_shadowed_trajectory(name, n_iter):
         w = max(r[1] for r in log[-4:])
         print(f"\n{name} iteration {it + 1}: worst projector err/bar {w:.3f}, injected-entrywise "
               f"{max(r[2] for r in log[-4:]):.2e}, own-move column {max(r[3] for r in log[-4:]):.2e}, "
-              f"e_V {e_gpu:.10f}, ISO fallbacks so far {fallbacks}")
+              f"e_V {e_gpu:.10f}, ISO fallbacks so far {fallbacks}"
+              + (f", warm-started solves {n_warm} (certified at the first check {n_hit}, cold retries {n_retry})"
+                 if warm else ""))
+    if warm:
+        assert n_warm > 0
 
 
 @pytest.mark.parametrize("name", ["c2", "c4"])
@@ -249,8 +262,9 @@ def test_reduced_env_with_injected_side_isometries(name):
     assert rel_err(M2.cpu().numpy(), M1.cpu().numpy()) <= 1e-14
 
 
-def test_c4_dl_20_iterations_against_the_golden_oracle_trajectory():
-    """BASELINE config 4's 20-iteration energy check on the converging variant c4_dl (D = 8,
+@pytest.mark.parametrize("warm", [False, True])
+def test_c4_dl_20_iterations_against_the_golden_oracle_trajectory(warm):
+    """(warm: with CTM_FLAG_WARM_START, same bars.)  BASELINE config 4's 20-iteration energy check on the converging variant c4_dl (D = 8,
     chi = 64, reading R16b): the GPU's gauge-invariant closures after every CTM iteration
     against the oracle's trajectory stored in tests/golden/oracle_c4_dl.json (written by
     tools/make_golden.py --dl from oracle/ only; the oracle's own perturbed-start spread on
@@ -261,7 +275,7 @@ def test_c4_dl_20_iterations_against_the_golden_oracle_trajectory():
     cfg = ci.CONFIGS["c4_dl"]
     g = ci.generate(cfg)
     A, B = T_(g["A"]), T_(g["B"])
-    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp)
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp, flags=ctm.CTM_FLAG_WARM_START if warm else 0)
     env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
     hop = T_(ci.heisenberg_h())
     worst, fails = {}, []
@@ -284,3 +298,41 @@ def test_c4_dl_20_iterations_against_the_golden_oracle_trajectory():
         print(f"iteration {it + 1}: " + ", ".join(line) + f", norm cancellation ratio {ratio:.2e}")
     print(f"c4_dl 20 iterations: worst relative deviation from the golden oracle trajectory {worst}")
     assert not fails, fails
+
+
+def test_warm_start_consecutive_left_moves_c4():
+    """CTM_FLAG_WARM_START at the headline config, in bench.py's own sequence (consecutive left
+    moves on one environment): the second move -- all ten truncating solves warm-started from the
+    first move's blocks -- shadowed by the oracle (projectors, injected-entrywise 1e-11, own-move
+    column 1e-9); no cuSOLVER fallback in the later moves (sites whose first check was wasted
+    back off, the right-side sites -- identical matrices in consecutive left moves -- keep
+    hitting), and ctm_warm_reset makes the next move cold again."""
+    cfg = ci.CONFIGS["c4"]
+    g = ci.generate(cfg)
+    A, B = g["A"], g["B"]
+    h = ctm.CtmHandle(cfg.d, cfg.D, cfg.chi, cfg.chi_p, cfg.chi_pp,
+                      flags=ctm.CTM_FLAG_CHECK_FINITE | ctm.CTM_FLAG_WARM_START)
+    env = ctm.Env.from_host(g["C"], g["T"], cfg.D, cfg.chi)
+    iso = torch.zeros(h.iso_numel(), dtype=torch.float64, device=DEV)
+    rng = np.random.default_rng(5)
+    log = []
+    for mv in range(5):
+        before = env.to_host() if mv == 1 else None
+        st = h.ctm_left_move(T_(A), T_(B), env, iso_out=iso)
+        assert st["n_svd_fallback"] == 0, (mv, st)
+        # 10 truncating solves per move (the second absorption reuses the right-side TS)
+        if mv == 0:
+            assert st["n_warm"] == 0
+        elif mv == 1:
+            assert st["n_warm"] == 10, st["n_warm"]
+        else:
+            assert 2 <= st["n_warm"] <= 10 and st["n_warm_hit"] >= 2, (mv, st["n_warm"], st["n_warm_hit"])
+        print(f"\nmove {mv + 1}: {st['ms_total']:.2f} ms, warm {st['n_warm']}, certified at the first check "
+              f"{st['n_warm_hit']}, cold retries {st['n_warm_retry']}")
+        if mv == 1:
+            shadow_move(before, A, B, "left", cfg, iso.cpu().numpy(), env.to_host(), rng, log)
+            print(f"move 2 shadowed: worst projector err/bar {log[0][1]:.3f}, injected-entrywise {log[0][2]:.2e}, "
+                  f"own-move column {log[0][3]:.2e}")
+    h.ctm_warm_reset()
+    st = h.ctm_left_move(T_(A), T_(B), env)
+    assert st["n_warm"] == 0 and st["n_svd_fallback"] == 0
