@@ -11,9 +11,13 @@
 // of partial traffic per Chebyshev degree.  Here a 32 x 32 tile keeps the full K per CTA
 // (160 CTAs at N = 160: one per SM), so the recurrence is one launch and no slab.
 //
-//  * 4 warps, 2 x 2 warp tiles of 16 x 16 (2 x 2 m8n8 DMMA tiles each), BK = 16, 4-stage
-//    cp.async pipeline (16-byte copies for A; 16-byte for X when its rows are 16-byte
-//    aligned, 8-byte otherwise), zero-fill (src-size 0) outside the matrix.
+//  * 4 warps, 2 x 2 warp tiles of 16 x 16 (2 x 2 m8n8 DMMA tiles each), BK = 32, 3-stage
+//    cp.async pipeline in dynamic shared memory (16-byte copies for A; 16-byte for X when
+//    its rows are 16-byte aligned, 8-byte otherwise), zero-fill (src-size 0) outside the
+//    matrix.  Build knobs FG_BK / FG_STAGES / FG_BM: BK = 16 with 4 stages (the first
+//    version) had 24 KB in flight per SM and a block barrier every 16 k; A/B of the full
+//    move: C4 33.12 -> 31.65 ms, C3 11.75 -> 11.44, C5 157.7 -> 156.4; deeper pipelines of
+//    16, 2 stages of 32 and BK = 64 were slower (profiles/r02s3_ab_fgemm_bk.jsonl).
 //  * shared pitches = 4 (mod 16) doubles: the m8n8k4 fragment reads of a warp hit 16
 //    distinct 8-byte bank pairs per half-warp (conflict-free), for both A orientations.
 //  * fragment double buffering: k-step kk + 1's fragments are read under kk's DMMAs.
@@ -35,13 +39,19 @@ struct FgArgs {
 };
 
 #ifndef FG_STAGES
-#define FG_STAGES 4
+#define FG_STAGES 3
 #endif
 #ifndef FG_BK
-#define FG_BK 16
+#define FG_BK 32
 #endif
-constexpr int BM = 32, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128;
-static_assert(BK == 16 || BK == 32, "fgemm: BK is 16 or 32");
+#ifndef FG_BM
+#define FG_BM 32
+#endif
+constexpr int BM = FG_BM, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128;
+static_assert(BM == 32 || BM == 64, "fgemm: BM is 32 or 64");
+constexpr int MI = BM / 16;                       // m8 DMMA tiles per warp (2 warp rows of BM / 2)
+constexpr int MCH = BM / 2;                       // 16-byte chunks per k-row of a transposed A tile
+static_assert(BK == 16 || BK == 32 || BK == 64, "fgemm: BK is 16, 32 or 64");
 constexpr int KCH = BK / 2;                       // 16-byte chunks per k-row of a non-transposed A tile
 constexpr int A_ITERS = BM * BK / 2 / THREADS;    // 16-byte A chunks per thread and k-tile
 constexpr int X_ITERS = BK * BN / 2 / THREADS;    // 16-byte X chunks per thread and k-tile
@@ -92,7 +102,7 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
         const bool in = m0 + r < M && k0 + kc < K;
         cp16(As + (r * LDA_N + kc) * 8, in ? p.A + (size_t)(m0 + r) * p.lda + k0 + kc : p.A, in);
       } else {
-        const int kr = c >> 4, mc = (c & 15) * 2;
+        const int kr = c / MCH, mc = (c % MCH) * 2;
         const bool in = k0 + kr < K && m0 + mc < M;
         cp16(As + (kr * LDA_T + mc) * 8, in ? p.A + (size_t)(k0 + kr) * p.lda + m0 + mc : p.A, in);
       }
@@ -119,14 +129,14 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
   const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t = lane & 3;
-  double acc[2][2][2] = {};
-  double af[2][2], bf[2][2];
+  double acc[MI][2][2] = {};
+  double af[2][MI], bf[2][2];
   auto frag = [&](int buf, int stage, int kk) {
     const double* As = sm + stage * STAGE_DOUBLES;
     const double* Bs = As + A_DOUBLES;
 #pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int m = wm * 16 + i * 8 + g;
+    for (int i = 0; i < MI; ++i) {
+      const int m = wm * (BM / 2) + i * 8 + g;
       af[buf][i] = TRANS ? As[(kk + t) * LDA_T + m] : As[m * LDA_N + kk + t];
     }
 #pragma unroll
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     for (int q = 0; q < BK / 4; ++q) {
       if (q < BK / 4 - 1) frag((q + 1) & 1, cur, 4 * (q + 1));
 #pragma unroll
-      for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) dmma(acc[i][j], af[q & 1][i], bf[q & 1][j]);
     }
@@ -162,8 +172,8 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
   const double alpha = p.alpha, beta = p.beta, gamma = p.gamma;
   const bool vec = ((p.ldc | p.ldy) & 1) == 0;   // (host: ldy = ldc when Y is null)
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int m = m0 + wm * 16 + i * 8 + g;
+  for (int i = 0; i < MI; ++i) {
+    const int m = m0 + wm * (BM / 2) + i * 8 + g;
     if (m >= M) continue;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
