@@ -138,6 +138,8 @@ struct Solver {
     double* S = h.ws.take((size_t)n * n);
     double* rd = h.ws.take((size_t)n);
     double* Rpk = n <= LMAX ? h.ws.take(rpk_size(n)) : nullptr;
+    // (tried: the Gram GEMM's split-K partials summed by chol_kernel's load instead of the reduction
+    // launch -- no change at C3/C4/C5, profiles/r02s3_ab_chol_defer.jsonl; PDL already hides it)
     gemm(Y, "ia", {m, n}, Y, "ib", {m, n}, S, "ab", {n, n});
     if (h.dry) {
       if (n > LMAX) chol_two_block(S, n, shift_factor, R, rd, replace);   // reserves its scratch
