@@ -47,14 +47,10 @@ struct FgArgs {
 #ifndef FG_BM
 #define FG_BM 32
 #endif
-#ifndef FG_KSPLIT
-#define FG_KSPLIT 1
-#endif
-// KSPLIT = 2: a second group of 4 warps takes the upper half of every k-tile (twice the warps per
-// SM behind the same loads); its accumulators are added to group 0's through shared memory at the end
-constexpr int KSPLIT = FG_KSPLIT;
-constexpr int BM = FG_BM, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128 * KSPLIT;
-static_assert(KSPLIT == 1 || KSPLIT == 2, "fgemm: KSPLIT is 1 or 2");
+// (tried: a second group of 4 warps per CTA on the upper half of every k-tile, accumulators added
+// through shared memory at the end -- twice the warps behind the same loads: C4 31.9 -> 35.9 ms,
+// C3 12.4 -> 13.8 ms, profiles/r02s3_ab_fgemm_ksplit.jsonl; removed)
+constexpr int BM = FG_BM, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128;
 static_assert(BM == 32 || BM == 64, "fgemm: BM is 32 or 64");
 constexpr int MI = BM / 16;                       // m8 DMMA tiles per warp (2 warp rows of BM / 2)
 constexpr int MCH = BM / 2;                       // 16-byte chunks per k-row of a transposed A tile
@@ -133,9 +129,7 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     }
   };
 
-  const int warp = (tid >> 5) & 3, lane = tid & 31;
-  const int kg = tid >> 7;                    // k group (0 when KSPLIT = 1)
-  const int kbase = kg * (BK / KSPLIT);
+  const int warp = tid >> 5, lane = tid & 31;
   const int wm = warp >> 1, wn = warp & 1;
   const int g = lane >> 2, t = lane & 3;
   double acc[MI][2][2] = {};
@@ -164,10 +158,10 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
     if (nk < ktiles) load(nk % STAGES, nk);
     commit();
     const int cur = kt % STAGES;
-    frag(0, cur, kbase);
+    frag(0, cur, 0);
 #pragma unroll
-    for (int q = 0; q < BK / 4 / KSPLIT; ++q) {
-      if (q < BK / 4 / KSPLIT - 1) frag((q + 1) & 1, cur, kbase + 4 * (q + 1));
+    for (int q = 0; q < BK / 4; ++q) {
+      if (q < BK / 4 - 1) frag((q + 1) & 1, cur, 4 * (q + 1));
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -176,28 +170,6 @@ __global__ void __launch_bounds__(THREADS) fgemm_kernel(const FgArgs p) {
   }
   wait_group<0>();
   CTM_PDL_TRIGGER();
-  if (KSPLIT == 2) {   // acc(group 0) += acc(group 1), through the drained pipeline buffers
-    __syncthreads();
-    double* red = sm + (size_t)(tid & 127) * (MI * 4);
-    if (kg == 1) {
-#pragma unroll
-      for (int i = 0; i < MI; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          red[(i * 2 + j) * 2] = acc[i][j][0];
-          red[(i * 2 + j) * 2 + 1] = acc[i][j][1];
-        }
-    }
-    __syncthreads();
-    if (kg == 1) return;
-#pragma unroll
-    for (int i = 0; i < MI; ++i)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        acc[i][j][0] += red[(i * 2 + j) * 2];
-        acc[i][j][1] += red[(i * 2 + j) * 2 + 1];
-      }
-  }
 
   // epilogue: C = alpha acc + beta Y + gamma W (accumulator pair = columns 2t, 2t + 1)
   const double alpha = p.alpha, beta = p.beta, gamma = p.gamma;
