@@ -347,7 +347,8 @@ double ctm_move_flops(int d, int D, int chi, int chi_p, int chi_pp);
 /* Number of libctm kernels launched since the handle was created (evidence counter). */
 int64_t ctm_kernel_count(ctm_handle h);
 
-/* CTM_FLAG_WARM_START: forget every solve site's stored block (the next move starts cold; the
+/* CTM_FLAG_WARM_START (the truncated SVDs of P:L60 / P:L145 across the N_CTM iterations of P:L48): forget
+ * every solve site's stored block (the next move starts cold; the
  * device buffers are kept for reuse).  Call it when A, B or the environment are replaced by
  * unrelated ones -- not required for correctness (every solve is certified on its own matrix),
  * only so that a stale block does not cost a failed warm solve.  CTM_OK also without the flag. */

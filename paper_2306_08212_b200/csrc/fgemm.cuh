@@ -50,6 +50,12 @@ struct FgArgs {
 // (tried: a second group of 4 warps per CTA on the upper half of every k-tile, accumulators added
 // through shared memory at the end -- twice the warps behind the same loads: C4 31.9 -> 35.9 ms,
 // C3 12.4 -> 13.8 ms, profiles/r02s3_ab_fgemm_ksplit.jsonl; removed)
+// (tried: warp-level split-K -- every warp the whole 32 x 32 tile over a quarter of each k-tile's
+// k-steps, 16 independent accumulators per warp and half the fragment loads, partial tiles summed
+// through shared memory; ncu on the kernel alone shows `wait` as the top stall and the DMMA pipe at
+// 49% (profiles/r02s3_ncu_solver_kernels.txt), but inside the move the concurrent solves already
+// hide that latency: C4 31.65 -> 32.0 ms, C5 156.8 -> 157.3 ms, profiles/r02s3_ab_fgemm_wsplit.jsonl;
+// removed)
 constexpr int BM = FG_BM, BN = 32, BK = FG_BK, STAGES = FG_STAGES, THREADS = 128;
 static_assert(BM == 32 || BM == 64, "fgemm: BM is 32 or 64");
 constexpr int MI = BM / 16;                       // m8 DMMA tiles per warp (2 warp rows of BM / 2)
