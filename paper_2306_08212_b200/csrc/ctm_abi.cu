@@ -1289,6 +1289,7 @@ void init_solver(Handle& h, const ctm_params* p) {
   ctm::tc_init_kernels();   // per-device attributes, before any worker thread exists
   ctm::iso_init_kernels();
   CTM_CUDA(cudaMalloc(&h.dev_scalars, 4096));
+  CTM_CUDA(cudaMallocHost(&h.pin, 8192));
   h.dev_info = reinterpret_cast<int*>(reinterpret_cast<char*>(h.dev_scalars) + 2048);
   for (auto& e : h.ev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
   for (auto& e : h.jev) CTM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDefault));
@@ -1307,6 +1308,8 @@ void destroy_handle(Handle& h) {
     if (e) cudaEventDestroy(e);
   for (auto& e : h.prof_ev) cudaEventDestroy(e);
   if (h.dev_scalars) cudaFree(h.dev_scalars);
+  if (h.pin) cudaFreeHost(h.pin);
+  h.pin = nullptr;
   if (h.owns_stream && h.stream) cudaStreamDestroy(h.stream);
   h.gesvdj_info = nullptr;
   h.solver_params = nullptr;

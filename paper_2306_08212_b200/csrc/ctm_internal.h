@@ -98,6 +98,8 @@ struct Handle {
   std::vector<char> host_buf;          // cuSOLVER host workspace
   int* dev_info = nullptr;              // cuSOLVER info (inside a small private alloc)
   double* dev_scalars = nullptr;        // small device scratch (norms etc.)
+  void* pin = nullptr;                  // 8 KB of pinned host memory: the ISO solver's status / Ritz values /
+                                        // residuals come back in one stream-ordered round trip per check
   cudaEvent_t ev[8]{};   // 2,3: svd timing; 4,5: isometry fork/join; 6,7: iso solver debug / K7 profile
   cudaEvent_t jev[2]{};  // ISO solver: the pending Jacobi launch (ms_jacobi)
   std::string last_error;

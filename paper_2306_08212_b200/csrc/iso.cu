@@ -310,8 +310,9 @@ struct Solver {
   }
   void check_status(const char* what) {
     if (h.dry) return;
-    int st[6] = {0, 0, 0, 0, 0, 0};
-    CTM_CUDA(cudaMemcpyAsync(st, status, sizeof(st), cudaMemcpyDeviceToHost, h.stream));
+    // pinned destination: a pageable one makes every such copy its own blocking round trip
+    int* st = static_cast<int*>(h.pin);
+    CTM_CUDA(cudaMemcpyAsync(st, status, 6 * sizeof(int), cudaMemcpyDeviceToHost, h.stream));
     CTM_CUDA(cudaStreamSynchronize(h.stream));
     last_sweeps = st[2];
     if (jac_pending) {
@@ -419,10 +420,11 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
       U = Ut;
     }
     signfix(h, U, n, 1, R, n_keep, out);
+    // (the singular values ride on check_status's synchronisation through the pinned buffer)
+    double* hp = reinterpret_cast<double*>(static_cast<char*>(h.pin) + 64);
+    CTM_CUDA(cudaMemcpyAsync(hp, S, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
     sv.check_status("iso direct");
-    std::vector<double> s(n);
-    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * n, cudaMemcpyDeviceToHost, h.stream));
-    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    std::vector<double> s(hp, hp + n);
     for (double x : s)
       if (!std::isfinite(x)) throw Error(CTM_E_NONFINITE, "non-finite singular value in a " + std::to_string(R) +
                                                                " x " + std::to_string(C) + " isometry");
@@ -600,12 +602,16 @@ static double iso_left(Handle& h, const double* mat, int R, int C, int n_keep, d
     CTM_CUDA(cudaGetLastError());
     h.count_kernel();
     if (debug) CTM_CUDA(cudaEventRecord(e_rr1, h.stream));
+    // Ritz values and residuals ride on check_status's synchronisation (one round trip per check
+    // through the handle's pinned buffer: 64 bytes of status, then la + ka <= 2 LMAX_BIG doubles)
+    double* hp = reinterpret_cast<double*>(static_cast<char*>(h.pin) + 64);
+    CTM_CUDA(cudaMemcpyAsync(hp, S, sizeof(double) * la, cudaMemcpyDeviceToHost, h.stream));
+    CTM_CUDA(cudaMemcpyAsync(hp + la, res, sizeof(double) * ka, cudaMemcpyDeviceToHost, h.stream));
     sv.check_status("iso subspace");
     if (debug) std::fprintf(stderr, "[iso]   check %d after %d degrees: active %d locked %d jacobi sweeps %d\n", checks,
                             degrees, la, nlock, sv.last_sweeps);
-    CTM_CUDA(cudaMemcpyAsync(s.data(), S, sizeof(double) * la, cudaMemcpyDeviceToHost, h.stream));
-    CTM_CUDA(cudaMemcpyAsync(r.data(), res, sizeof(double) * ka, cudaMemcpyDeviceToHost, h.stream));
-    CTM_CUDA(cudaStreamSynchronize(h.stream));
+    std::copy(hp, hp + la, s.begin());
+    std::copy(hp + la, hp + la + ka, r.begin());
     if (debug) {
       float ms = 0.f;
       CTM_CUDA(cudaEventElapsedTime(&ms, e_rr0, e_rr1));
